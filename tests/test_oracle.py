@@ -1,0 +1,209 @@
+"""Pins for the CPU oracle (oracle/), CPU only.
+
+Each oracle function is checked against something other than itself:
+brute force over permutation-row stackings for N <= 5, the N!
+first-row invariant, the vertical-symmetry definition
+checked square by square, Fig. 1 and the hourglass count of P:436.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, paper_counts
+
+
+def fig1():
+    rows = []
+    with open(golden("fig1_dls9_order.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            rows.append([int(x) for x in line.split()])
+    return np.array(rows)
+
+
+# ------------------------------------------------------------------ definitions
+
+def test_definitions_on_hand_examples():
+    # a DLS of order 4 with row 0 = 0123, checked by hand
+    sq = np.array([[0, 1, 2, 3], [2, 3, 0, 1], [3, 2, 1, 0], [1, 0, 3, 2]])
+    assert oracle.is_latin(sq) and oracle.is_diagonal(sq)
+    # rows are vertically symmetric: 0+3 = 1+2 = 3 etc.
+    assert oracle.is_vertically_symmetric(sq)
+    bad = sq.copy()
+    bad[1], bad[2] = sq[2].copy(), sq[1].copy()      # still Latin, breaks main diagonal
+    assert oracle.is_latin(bad) and not oracle.is_diagonal(bad)
+    cyc = np.array([[(i + j) % 4 for j in range(4)] for i in range(4)])
+    assert oracle.is_latin(cyc) and not oracle.is_diagonal(cyc)
+
+
+def test_brute_force_latin_counts():
+    # the brute force itself: Latin squares (no diagonal filter) of orders 1..5
+    # are 1, 2, 12, 576, 161280 in total; with row 0 fixed divide by N!.
+    for n, total in ((1, 1), (2, 2), (3, 12), (4, 576)):
+        assert oracle.brute_force_count(n, diagonal=False, fixed_first_row=False) == total
+    assert oracle.brute_force_count(5, diagonal=False, fixed_first_row=True) == 161280 // 120
+
+
+# ------------------------------------------------------------------ plan (Section 2.3)
+
+def test_plan_reproduces_fig1():
+    n = 9
+    order = oracle.plan(n)
+    got = np.zeros((n, n), dtype=int)
+    for step, cell in enumerate(order):
+        got[cell // n, cell % n] = step + 1
+    assert (got[1:] == fig1()).all()
+
+
+@pytest.mark.parametrize("n", range(1, 11))
+@pytest.mark.parametrize("fixed", [True, False])
+def test_plan_is_permutation_of_free_cells(n, fixed):
+    pre = np.zeros((n, n), dtype=np.int32)
+    if fixed:
+        pre[0, :] = 1
+    order = oracle.plan(n, False, pre)
+    assert sorted(order) == [c for c in range(n * n) if not pre.reshape(-1)[c]]
+
+
+@pytest.mark.parametrize("n", [4, 6, 8, 10])
+def test_vs_plan_covers_left_half(n):
+    order = oracle.plan(n, True)
+    assert sorted(order) == [i * n + j for i in range(1, n) for j in range(n // 2)]
+
+
+@pytest.mark.parametrize("n", range(5, 11))
+def test_plan_puts_diagonals_first(n):
+    # P:174 "we start with diagonal elements, and then fill the rest"
+    order = oracle.plan(n)
+    diag = {i * n + j for i in range(1, n) for j in range(n) if i == j or i + j == n - 1}
+    assert set(order[:len(diag)]) == diag
+
+
+def test_plan_forced_cells_are_forced():
+    # a cell taken because its unit reached N-1 assigned cells really is
+    # the last free cell of that unit at that step (replay check).
+    n = 9
+    order = oracle.plan(n)
+    a = np.zeros((n, n), dtype=int)
+    a[0, :] = 1
+    forced_steps = 0
+    for cell in order:
+        i, j = divmod(cell, n)
+        units = [a[i, :].sum(), a[:, j].sum()]
+        if i == j:
+            units.append(sum(a[k, k] for k in range(n)))
+        if i + j == n - 1:
+            units.append(sum(a[k, n - 1 - k] for k in range(n)))
+        if max(units) == n - 1:
+            forced_steps += 1
+        a[i, j] = 1
+    # Fig. 1: the last cell of each of rows 1..8 and both diagonals is forced at least
+    assert forced_steps >= 10
+
+
+# ------------------------------------------------------------------ counts vs brute force
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_count_matches_brute_force_first_row_fixed(n):
+    assert oracle.count_all(n, fixed_first_row=True) == oracle.brute_force_count(n, True, False, True)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_count_matches_brute_force_free(n):
+    assert oracle.count_all(n, fixed_first_row=False) == oracle.brute_force_count(n, True, False, False)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_vs_count_matches_brute_force(n, fixed):
+    assert oracle.count_all(n, vs=True, fixed_first_row=fixed) == \
+        oracle.brute_force_count(n, True, True, fixed)
+
+
+@pytest.mark.parametrize("n", [4, 5])
+def test_squares_equal_brute_force_set(n):
+    # not only the number: the very same squares
+    got = oracle.squares(n, False, oracle.first_row_grid(n))
+    want = oracle.brute_force_squares(n, True, False, True)
+    key = lambda s: tuple(np.asarray(s).reshape(-1).tolist())
+    assert sorted(map(key, got)) == sorted(map(key, want))
+    assert all(oracle.is_diagonal(s) for s in got)
+
+
+# ------------------------------------------------------------------ invariants
+
+@pytest.mark.parametrize("n", [4, 5, 6])
+def test_first_row_factor_is_n_factorial(n):
+    # renaming symbols maps DLS to DLS bijectively, so total = N! * (row 0 fixed)
+    assert oracle.count_all(n, fixed_first_row=False) == \
+        math.factorial(n) * oracle.count_all(n, fixed_first_row=True)
+
+
+@pytest.mark.parametrize("n", [4, 6])
+def test_vs_first_row_factor(n):
+    # reading R3: only renamings commuting with x -> N-1-x keep vertical symmetry
+    assert oracle.count_all(n, vs=True, fixed_first_row=False) == \
+        oracle.vs_first_row_multiplier(n) * oracle.count_all(n, vs=True, fixed_first_row=True)
+
+
+@pytest.mark.parametrize("n", [4, 6])
+def test_vs_squares_by_definition(n):
+    """VS enumeration == DLS enumeration filtered by LS[i][j]+LS[i][N-1-j]=N-1."""
+    g = oracle.first_row_grid(n)
+    vs_sq = oracle.squares(n, True, g)
+    assert len(vs_sq) == oracle.count_all(n, vs=True)
+    for s in vs_sq:
+        assert oracle.is_diagonal(s) and oracle.is_vertically_symmetric(s)
+    all_sq = oracle.squares(n, False, g)
+    filt = [s for s in all_sq if oracle.is_vertically_symmetric(s)]
+    key = lambda s: tuple(np.asarray(s).reshape(-1).tolist())
+    assert sorted(map(key, filt)) == sorted(map(key, vs_sq))
+
+
+def test_odd_order_has_no_vs_squares():
+    for n in (3, 5, 7):
+        assert oracle.count_all(n, vs=True) == 0
+
+
+@pytest.mark.parametrize("n,depth", [(6, 8), (7, 12), (7, 14)])
+def test_prefix_additivity(n, depth):
+    """Workunits partition the search: sum over all depth-k prefixes of
+    their completions equals the count, and nodes add up level by level."""
+    g = oracle.first_row_grid(n)
+    order = oracle.plan(n)
+    total, nodes = oracle.count(n, False, g, order)
+    pre = oracle.prefixes(n, False, g, order, depth)
+    parts = [oracle.count(n, False, p, order[depth:]) for p in pre]
+    assert sum(c for c, _ in parts) == total
+    upper = sum(oracle.count_prefixes(n, False, g, order, d) for d in range(1, depth + 1))
+    assert upper + sum(nd for _, nd in parts) == nodes
+
+
+def test_count_is_order_independent():
+    # the count is a property of the partial square, not of the cell order
+    n = 6
+    g = oracle.first_row_grid(n)
+    a = oracle.count(n, False, g)[0]
+    b = oracle.count(n, False, g, [c for c in range(n, n * n)])[0]          # row-major
+    c = oracle.count(n, False, g, list(reversed(range(n, n * n))))[0]
+    assert a == b == c > 0
+
+
+def test_inconsistent_grid_counts_zero():
+    g = oracle.first_row_grid(5)
+    g[1, 1] = 1          # column 1 already holds 1
+    assert oracle.count(5, False, g)[0] == 0
+
+
+def test_hourglass_count_order8():
+    """'for diagonal Latin squares of order N=8 it is equal to 22 192 248'
+    hourglass designs (row 0, row N-1 and both diagonals assigned)."""
+    n = 8
+    g = oracle.first_row_grid(n)
+    diag = [i * n + j for i in range(1, n) for j in range(n) if i == j or i + j == n - 1]
+    last = [(n - 1) * n + j for j in range(n) if (n - 1) * n + j not in diag]
+    assert oracle.count_prefixes(n, False, g, diag + last, len(diag) + len(last)) == \
+        paper_counts()["hourglass8"]
