@@ -1,0 +1,135 @@
+/*
+ * dls_b200.h -- C ABI of the B200 (sm_100a) diagonal-Latin-square enumerator.
+ *
+ * Implements the data-parallel hot path of Kochemazov, Vatutin, Zaikin, "Fast
+ * Algorithm for Enumerating Diagonal Latin Squares of Small Order"
+ * (arXiv:1709.02599).  "P:<n>" cites line n of the paper's PAPER.md.
+ *
+ * Terms
+ *   order n        1 <= n <= 10 (the paper's range: "order at most 9 ... 10").
+ *   symmetric      0 = diagonal Latin squares (DLS);
+ *                  1 = vertically symmetric DLS, LS[i][j] = n-1-LS[i][n-1-j]
+ *                      (P:520-522); even n only.
+ *   fixed_first_row 1 = row 0 is assigned a priori to 0..n-1 (normalisation);
+ *                  0 = row 0 is searched like every other row.
+ *   plan           the cell order of Section 2.3: repeatedly take the
+ *                  last free cell of any row/column/diagonal with n-1 assigned
+ *                  cells (rows, then columns, then main diagonal, then antidiagonal),
+ *                  else the free cell with the largest V = r_i + c_j + md + ad,
+ *                  lexicographically first among ties.  For symmetric=1 only
+ *                  left-half cells (j <= n-1-j) are planned; taking (i,j) also
+ *                  assigns its mirror (i,n-1-j) (reading R4).
+ *   prefix record  n*n bytes, row-major, cell value 0..n-1 or DLS_EMPTY (0xFF).
+ *                  A depth-d prefix assigns exactly row 0 (if fixed_first_row),
+ *                  the first d plan cells (and their mirrors when symmetric), and
+ *                  nothing else: a workunit of P:481.
+ *   diag depth     the smallest d whose prefixes assign every cell of the main
+ *                  diagonal and antidiagonal.  dls_count needs depth >= diag depth
+ *                  (the GPU search then only tracks row and column sets).
+ *   count          number of complete (symmetric) DLS that extend a prefix.
+ *   node           a consistent partial square visited below a prefix (each
+ *                  successful cell assignment, leaves included); the unit of
+ *                  "search nodes/sec".
+ *
+ * Error behaviour: every call returns a negative DLS_E_* code on failure and
+ * writes nothing it did not document as written.  No call aborts the process.
+ * Thread safety: calls are reentrant; dls_count serialises on its own stream.
+ */
+#ifndef DLS_B200_H
+#define DLS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DLS_EMPTY 0xFF
+#define DLS_MAX_ORDER 10
+
+#define DLS_OK 0
+#define DLS_E_ARG (-1)         /* bad order / depth / flag / null pointer        */
+#define DLS_E_CUDA (-2)        /* a CUDA runtime call failed (see dls_last_error) */
+#define DLS_E_PREFIX (-3)      /* a prefix record is not a consistent depth-d prefix */
+#define DLS_E_NODEVICE (-4)    /* no CUDA device: the GPU path is the only path  */
+
+/* Version string of the library ("dls_b200 <semver> sm_100a"). */
+const char *dls_version(void);
+
+/* Human-readable text of the last error on the calling thread ("" if none). */
+const char *dls_last_error(void);
+
+/*
+ * dls_plan -- the Section 2.3 cell order (Fig. 1 for n = 9).
+ *   out_cells      host, capacity n*n int32: cells as i*n+j in fill order
+ *                  (row 0 excluded when fixed_first_row; left half only when
+ *                  symmetric).
+ *   out_forced     host, capacity n*n uint8 or NULL: 1 where the step was taken
+ *                  by the forced-cell rule of P:154 / Section 2.4.1.
+ *   out_n_steps    host: number of cells written.
+ *   out_diag_depth host: diag depth (see Terms).
+ * Returns DLS_OK or DLS_E_ARG.
+ */
+int dls_plan(int n, int symmetric, int fixed_first_row,
+             int32_t *out_cells, uint8_t *out_forced,
+             int32_t *out_n_steps, int32_t *out_diag_depth);
+
+/*
+ * dls_split -- the workunit decomposition of P:481: every consistent assignment
+ * of the first `depth` plan cells (0 <= depth <= n_steps), in depth-first order
+ * with candidate values increasing at every cell (rightmost-bit order of Alg. 4,
+ * P:242-243).
+ *   out_prefixes   host, capacity*n*n bytes (prefix records) or NULL.
+ *   capacity       number of records out_prefixes can hold.
+ * Writes min(total, capacity) records and returns total (int64, may exceed
+ * capacity: call with NULL/0 first to size the buffer), or a DLS_E_* code.
+ */
+int64_t dls_split(int n, int symmetric, int fixed_first_row, int depth,
+                  uint8_t *out_prefixes, int64_t capacity);
+
+/*
+ * dls_count -- exhaustive completion count of every prefix (Alg. 4, P:235-258,
+ * run on the B200: one prefix per lane of a persistent sm_100a kernel, an
+ * explicit per-lane stack, a global atomic work queue and warp-level subtree
+ * donation).
+ *   prefix_buf     n_prefix depth-`depth` prefix records; host or device memory
+ *                  (detected; host buffers are staged to the device inside the call).
+ *   out_counts     n_prefix uint64 completion counts (host or device) or NULL.
+ *   out_total      host uint64: sum of all counts, or NULL.
+ *   out_nodes      host uint64: search nodes visited, or NULL.
+ *   stream         cudaStream_t to run on (NULL = legacy default stream).
+ * Synchronous: returns after the results are written.  Returns DLS_OK,
+ * DLS_E_ARG (depth < diag depth, bad sizes), DLS_E_PREFIX (some record is not a
+ * consistent depth-`depth` prefix; its count is 0), DLS_E_CUDA, DLS_E_NODEVICE.
+ */
+int dls_count(int n, int symmetric, int fixed_first_row, int depth,
+              const uint8_t *prefix_buf, int64_t n_prefix,
+              uint64_t *out_counts, uint64_t *out_total, uint64_t *out_nodes,
+              void *stream);
+
+/*
+ * dls_count_async -- the same search, enqueued on `stream` without waiting.
+ * All pointers are DEVICE memory:
+ *   d_prefixes     n_prefix prefix records.
+ *   d_counts       n_prefix uint64 or NULL (zeroed by the call).
+ *   d_stats        DLS_STATS_WORDS uint64 (zeroed by the call); after the stream
+ *                  completes: [0] total count, [1] nodes, [2] prefix-error flag
+ *                  (nonzero = some record was inconsistent), [3] work-queue
+ *                  cursor, [4] subtree donations, [5..7] reserved.
+ * Returns DLS_OK or DLS_E_ARG/DLS_E_CUDA/DLS_E_NODEVICE for launch-time errors.
+ */
+#define DLS_STATS_WORDS 8
+int dls_count_async(int n, int symmetric, int fixed_first_row, int depth,
+                    const uint8_t *d_prefixes, int64_t n_prefix,
+                    uint64_t *d_counts, uint64_t *d_stats, void *stream);
+
+/*
+ * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
+ * per call (for the bench's launch count): the search kernel only.
+ */
+int dls_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLS_B200_H */

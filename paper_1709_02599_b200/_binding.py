@@ -1,0 +1,143 @@
+"""Thin ctypes binding of libdls_b200.so (argument marshalling only).
+
+Names follow the C ABI in include/dls_b200.h.  Every step of the search runs in
+the library's CUDA kernel; there is no Python or CPU fallback: on a machine
+without a GPU ``dls_count`` raises ``DlsError(DLS_E_NODEVICE)``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import build as _build
+
+DLS_EMPTY = 0xFF
+DLS_MAX_ORDER = 10
+DLS_STATS_WORDS = 8
+DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
+
+EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_count",
+           "dls_count_async", "dls_kernel_launches")
+
+_lib = None
+
+
+class DlsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__("%s (code %d)" % (msg, code))
+        self.code = code
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load the in-tree library (building it first if it is missing or stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if build_if_missing and (not os.path.exists(path) or _build._stale()):
+        _build.build()
+    if not os.path.exists(path):
+        raise DlsError(DLS_E_NODEVICE, "libdls_b200.so is missing: run paper_1709_02599_b200.build")
+    lib = ctypes.CDLL(path)
+    c_int, c_i64, vp = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+    lib.dls_version.restype = ctypes.c_char_p
+    lib.dls_last_error.restype = ctypes.c_char_p
+    lib.dls_plan.argtypes = [c_int, c_int, c_int, vp, vp, vp, vp]
+    lib.dls_plan.restype = c_int
+    lib.dls_split.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64]
+    lib.dls_split.restype = c_i64
+    lib.dls_count.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp, vp]
+    lib.dls_count.restype = c_int
+    lib.dls_count_async.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp]
+    lib.dls_count_async.restype = c_int
+    lib.dls_kernel_launches.restype = c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str):
+    if rc < 0:
+        raise DlsError(int(rc), "%s: %s" % (what, load().dls_last_error().decode()))
+
+
+def dls_version() -> str:
+    return load().dls_version().decode()
+
+
+def dls_plan(n: int, symmetric: bool = False, fixed_first_row: bool = True):
+    """-> (cells[int32], forced[uint8], diag_depth)  (Section 2.3)."""
+    cells = np.zeros(n * n, dtype=np.int32)
+    forced = np.zeros(n * n, dtype=np.uint8)
+    steps = ctypes.c_int32(0)
+    dd = ctypes.c_int32(0)
+    rc = load().dls_plan(n, int(symmetric), int(fixed_first_row), cells.ctypes.data, forced.ctypes.data,
+                         ctypes.addressof(steps), ctypes.addressof(dd))
+    _check(rc, "dls_plan")
+    return cells[:steps.value].copy(), forced[:steps.value].copy(), int(dd.value)
+
+
+def dls_split(n: int, depth: int, symmetric: bool = False, fixed_first_row: bool = True) -> np.ndarray:
+    """All depth-`depth` prefix records, shape (count, n, n) uint8."""
+    lib = load()
+    total = lib.dls_split(n, int(symmetric), int(fixed_first_row), depth, None, 0)
+    _check(total, "dls_split")
+    out = np.empty((max(total, 1), n, n), dtype=np.uint8)
+    got = lib.dls_split(n, int(symmetric), int(fixed_first_row), depth, out.ctypes.data, total)
+    _check(got, "dls_split")
+    return out[:total]
+
+
+def _ptr(a) -> Tuple[int, object]:
+    """(address, keepalive) of a numpy array or a torch tensor (host or CUDA)."""
+    if a is None:
+        return 0, None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, a
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), a
+    raise TypeError("expected numpy array or torch tensor")
+
+
+def dls_count(n: int, depth: int, prefixes, symmetric: bool = False, fixed_first_row: bool = True,
+              out_counts=None, stream: Optional[int] = None) -> Tuple[int, int]:
+    """Count completions of every prefix on the GPU -> (total, nodes).
+
+    ``prefixes``: (count, n, n) uint8 records, numpy (host) or torch (host or cuda).
+    ``out_counts``: optional uint64 numpy array / int64 torch tensor of length count.
+    ``stream``: cudaStream_t handle (e.g. ``torch.cuda.current_stream().cuda_stream``).
+    """
+    n_prefix = int(prefixes.shape[0]) if prefixes is not None else 0
+    pp, keep1 = _ptr(prefixes)
+    cp, keep2 = _ptr(out_counts)
+    tot = ctypes.c_uint64(0)
+    nodes = ctypes.c_uint64(0)
+    rc = load().dls_count(n, int(symmetric), int(fixed_first_row), depth, pp or None, n_prefix, cp or None,
+                          ctypes.addressof(tot), ctypes.addressof(nodes), stream or None)
+    _check(rc, "dls_count")
+    return int(tot.value), int(nodes.value)
+
+
+def dls_count_async(n: int, depth: int, d_prefixes, d_counts, d_stats, symmetric: bool = False,
+                    fixed_first_row: bool = True, stream: Optional[int] = None) -> None:
+    """Enqueue the search on ``stream``; all tensors must be CUDA tensors."""
+    pp, k1 = _ptr(d_prefixes)
+    cp, k2 = _ptr(d_counts)
+    sp, k3 = _ptr(d_stats)
+    rc = load().dls_count_async(n, int(symmetric), int(fixed_first_row), depth, pp or None,
+                                int(d_prefixes.shape[0]), cp or None, sp, stream or None)
+    _check(rc, "dls_count_async")
+
+
+def dls_kernel_launches() -> int:
+    return int(load().dls_kernel_launches())

@@ -1,0 +1,40 @@
+// internal.h -- host-side helpers shared by the product's C++/CUDA sources.
+// (Product side only; the oracle under oracle/ shares nothing with this.)
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dls_b200.h"
+
+namespace dls {
+
+// Section 2.3 plan of a problem.
+struct Plan {
+    int n = 0;
+    bool vs = false;
+    bool fixed_first_row = false;
+    std::vector<int> cells;      // i*n+j in fill order
+    std::vector<uint8_t> forced; // 1 = taken by the forced-cell rule
+    int diag_depth = 0;          // first depth covering both diagonals
+};
+
+// Returns false on bad arguments.
+bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out);
+
+// Validity of (n, symmetric) combinations.
+bool valid_problem(int n, int symmetric, int fixed_first_row);
+
+// Children of `n_in` depth-d0 records at depth d1 (plan cells [d0, d1)), with
+// the index of their parent record.  Writes up to `capacity` records, returns the
+// total.  extra_nodes (optional) = partial squares at depths d0+1 .. d1.
+int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in, uint8_t *out,
+               uint32_t *parent, int64_t capacity, int64_t *extra_nodes);
+
+// Host-side check that a record is a consistent depth-`depth` prefix of `plan`.
+bool valid_record(const Plan &plan, int depth, const uint8_t *rec);
+
+void set_error(const std::string &msg);
+const char *get_error();
+
+}  // namespace dls

@@ -1,0 +1,208 @@
+// split.cpp -- host-side prefix splitter (workunit decomposition).
+//
+// Enumerates every consistent assignment of plan cells [d0, d1) below a start
+// grid with the bit-arithmetic loop of Alg. 4:
+//   CR = Rows[i] | Columns[j] | MD | AD        (MD/AD only on the diagonals)
+//   L  = AllN ^ CR, iterate b = L & -L, L &= L-1   (AllN = (1<<N)-1, reading R7)
+// For vertical symmetry assigning v at (i,j) also assigns N-1-v at
+// (i,N-1-j); both cells' constraints are folded into one candidate mask by
+// reflecting the mirror cell's forbidden set (bit v <-> bit N-1-v).
+//
+// dls_split     : from the empty / first-row grid, cells [0, depth)
+// dls::refine   : from given depth-d0 records, cells [d0, d1), with parent index
+//                 (used by dls_count to cut few large workunits into many)
+// dls::valid_record : host check of one record against a depth-d pattern
+#include <cstring>
+#include <functional>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+inline uint32_t reflect(uint32_t m, int n) {
+    uint32_t r = 0;
+    for (int v = 0; v < n; ++v)
+        if (m & (1u << v)) r |= 1u << (n - 1 - v);
+    return r;
+}
+
+class Enumerator {
+  public:
+    Enumerator(const dls::Plan &plan, int d0, int d1) : plan_(plan), n_(plan.n), d0_(d0), d1_(d1) {
+        all_n_ = (1u << n_) - 1u;
+        for (int k = d0; k < d1; ++k) {
+            ci_.push_back(plan.cells[k] / n_);
+            cj_.push_back(plan.cells[k] % n_);
+            cjm_.push_back(plan.vs ? n_ - 1 - plan.cells[k] % n_ : plan.cells[k] % n_);
+        }
+    }
+
+    // Load a start grid; returns false if its assigned cells are inconsistent.
+    bool load(const uint8_t *g) {
+        std::memcpy(grid_, g, n_ * n_);
+        std::memset(rows_, 0, sizeof(rows_));
+        std::memset(cols_, 0, sizeof(cols_));
+        md_ = ad_ = 0;
+        for (int i = 0; i < n_; ++i)
+            for (int j = 0; j < n_; ++j) {
+                const uint8_t v = grid_[i * n_ + j];
+                if (v == DLS_EMPTY) continue;
+                if (v >= n_) return false;
+                const uint32_t b = 1u << v;
+                if ((rows_[i] & b) || (cols_[j] & b)) return false;
+                if (i == j && (md_ & b)) return false;
+                if (i + j == n_ - 1 && (ad_ & b)) return false;
+                mark(i, j, b);
+            }
+        return true;
+    }
+
+    // Depth-first over cells [d0, d1); calls emit(grid) at depth d1 and counts,
+    // per relative level, the consistent partial squares visited.
+    template <class F>
+    void run(F &&emit, std::vector<int64_t> *level_nodes) {
+        const int depth = d1_ - d0_;
+        if (depth == 0) { emit(grid_); return; }
+        std::vector<uint32_t> L(depth), A(depth);
+        int k = 0;
+        L[0] = candidates(0);
+        while (k >= 0) {
+            if (L[k] == 0) {
+                if (--k < 0) break;
+                unassign(k, A[k]);
+                continue;
+            }
+            const uint32_t b = L[k] & (0u - L[k]);   // isolate rightmost 1-bit
+            L[k] &= L[k] - 1;                         // switch it off
+            A[k] = b;
+            assign(k, b);
+            if (level_nodes) (*level_nodes)[k]++;
+            if (k + 1 == depth) {
+                emit(grid_);
+                unassign(k, b);
+            } else {
+                ++k;
+                L[k] = candidates(k);
+            }
+        }
+    }
+
+  private:
+    void mark(int i, int j, uint32_t b) {
+        rows_[i] ^= b;
+        cols_[j] ^= b;
+        if (i == j) md_ ^= b;
+        if (i + j == n_ - 1) ad_ ^= b;
+    }
+    uint32_t forbidden(int i, int j) const {
+        return rows_[i] | cols_[j] | (i == j ? md_ : 0u) | (i + j == n_ - 1 ? ad_ : 0u);
+    }
+    uint32_t candidates(int k) const {
+        const int i = ci_[k], j = cj_[k];
+        uint32_t cr = forbidden(i, j);
+        if (plan_.vs && cjm_[k] != j) cr |= reflect(forbidden(i, cjm_[k]), n_);
+        return all_n_ ^ (cr & all_n_);
+    }
+    void assign(int k, uint32_t b) {
+        const int i = ci_[k], j = cj_[k];
+        const int v = __builtin_ctz(b);
+        mark(i, j, b);
+        grid_[i * n_ + j] = (uint8_t)v;
+        if (plan_.vs && cjm_[k] != j) {
+            mark(i, cjm_[k], 1u << (n_ - 1 - v));
+            grid_[i * n_ + cjm_[k]] = (uint8_t)(n_ - 1 - v);
+        }
+    }
+    void unassign(int k, uint32_t b) {
+        const int i = ci_[k], j = cj_[k];
+        const int v = __builtin_ctz(b);
+        mark(i, j, b);
+        grid_[i * n_ + j] = DLS_EMPTY;
+        if (plan_.vs && cjm_[k] != j) {
+            mark(i, cjm_[k], 1u << (n_ - 1 - v));
+            grid_[i * n_ + cjm_[k]] = DLS_EMPTY;
+        }
+    }
+
+    const dls::Plan &plan_;
+    int n_, d0_, d1_;
+    uint32_t all_n_;
+    std::vector<int> ci_, cj_, cjm_;
+    uint8_t grid_[DLS_MAX_ORDER * DLS_MAX_ORDER];
+    uint32_t rows_[DLS_MAX_ORDER], cols_[DLS_MAX_ORDER], md_, ad_;
+};
+
+}  // namespace
+
+namespace dls {
+
+int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in, uint8_t *out,
+               uint32_t *parent, int64_t capacity, int64_t *extra_nodes) {
+    const int nn = plan.n * plan.n;
+    Enumerator en(plan, d0, d1);
+    std::vector<int64_t> lv(d1 - d0 + 1, 0);
+    int64_t total = 0;
+    for (int64_t p = 0; p < n_in; ++p) {
+        if (!en.load(in + p * nn)) continue;   // inconsistent: no children
+        en.run(
+            [&](const uint8_t *g) {
+                if (total < capacity) {
+                    std::memcpy(out + total * nn, g, nn);
+                    if (parent) parent[total] = (uint32_t)p;
+                }
+                ++total;
+            },
+            &lv);
+    }
+    if (extra_nodes) {
+        // partial squares at depths d0+1 .. d1 (the new records included) are
+        // search nodes of the original workunits that lie above the new records
+        int64_t s = 0;
+        for (int k = 0; k < d1 - d0; ++k) s += lv[k];
+        *extra_nodes = s;
+    }
+    return total;
+}
+
+bool valid_record(const Plan &plan, int depth, const uint8_t *rec) {
+    const int n = plan.n;
+    bool want[DLS_MAX_ORDER * DLS_MAX_ORDER] = {};
+    if (plan.fixed_first_row)
+        for (int j = 0; j < n; ++j) want[j] = true;
+    for (int s = 0; s < depth; ++s) {
+        const int c = plan.cells[s];
+        want[c] = true;
+        if (plan.vs) want[(c / n) * n + (n - 1 - c % n)] = true;
+    }
+    for (int c = 0; c < n * n; ++c)
+        if ((rec[c] != DLS_EMPTY) != want[c]) return false;
+    if (plan.vs)
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                if (rec[i * n + j] != DLS_EMPTY && rec[i * n + (n - 1 - j)] != n - 1 - rec[i * n + j])
+                    return false;
+    Enumerator en(plan, depth, depth);
+    return en.load(rec);
+}
+
+}  // namespace dls
+
+extern "C" int64_t dls_split(int n, int symmetric, int fixed_first_row, int depth,
+                             uint8_t *out_prefixes, int64_t capacity) {
+    dls::Plan plan;
+    if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
+        dls::set_error("dls_split: unsupported (n, symmetric, fixed_first_row)");
+        return DLS_E_ARG;
+    }
+    if (depth < 0 || depth > (int)plan.cells.size() || capacity < 0 ||
+        (capacity > 0 && !out_prefixes)) {
+        dls::set_error("dls_split: bad depth / capacity");
+        return DLS_E_ARG;
+    }
+    uint8_t root[DLS_MAX_ORDER * DLS_MAX_ORDER];
+    std::memset(root, DLS_EMPTY, sizeof(root));
+    if (fixed_first_row)
+        for (int j = 0; j < n; ++j) root[j] = (uint8_t)j;
+    return dls::refine(plan, 0, depth, root, 1, out_prefixes, nullptr, capacity, nullptr);
+}

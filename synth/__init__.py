@@ -15,6 +15,12 @@ import numpy as np
 
 EMPTY = 0xFF
 
+# Fixed seeds of BASELINE.json's sampled configs.
+SEED_VS10 = 1709        # config 4: 4096 vertically symmetric order-10 prefixes
+SEED_DLS9 = 2599        # config 5: 1024 order-9 prefixes
+N_VS10 = 4096
+N_DLS9 = 1024
+
 
 def _consistent(g: np.ndarray) -> bool:
     """No value repeated among the assigned cells of a row, column, or diagonal."""

@@ -1,0 +1,256 @@
+"""GPU parity: the sm_100a kernel (through the C ABI) against the CPU oracle.
+
+Bar: counts are integers, so every comparison is bit-exact.
+Node counts are compared too wherever the oracle enumerates the same tree (same
+Section 2.3 order below the same prefixes).  The five BASELINE.json configs:
+
+  1  N=6, no first-row fixing: every prefix and the total
+  2  N=7, first row fixed: every prefix, total and the N! scaled total
+  3  N=8, first row fixed: full count = 7 447 587 840, sampled prefixes
+  4  VS N=8 full (every prefix) and VS N=10 on 4096 seeded prefixes
+  5  N=9 on 1024 seeded prefixes
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+import paper_1709_02599_b200 as D
+from paper_1709_02599_b200 import _binding as B
+from conftest import golden, paper_counts
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_per_prefix(n, vs, recs, depth, fixed=True):
+    pre = np.zeros((n, n), np.int32)
+    if fixed:
+        pre[0, :] = 1
+    order = oracle.plan(n, vs, pre)[depth:]
+    out = [oracle.count(n, vs, synth.to_int_grid(r), order) for r in recs]
+    return np.array([c for c, _ in out], dtype=np.uint64), sum(nd for _, nd in out)
+
+
+def _gpu(n, vs, recs, depth, fixed=True):
+    counts, total, nodes = D.count_prefixes(n, recs, vs, fixed, depth)
+    assert int(counts.sum()) == total
+    return counts, total, nodes
+
+
+# ------------------------------------------------------------------ config 1
+
+def test_config1_dls6_no_symmetry_breaking():
+    n, vs, fixed = 6, False, False
+    d = D.default_split_depth(n, vs, fixed)
+    recs = D.dls_split(n, d, vs, fixed)
+    counts, total, nodes = _gpu(n, vs, recs, d, fixed)
+    want, want_nodes = _oracle_per_prefix(n, vs, recs, d, fixed)
+    assert (counts == want).all()
+    assert nodes == want_nodes
+    assert total == oracle.count_all(n, fixed_first_row=False)
+    assert total == math.factorial(n) * oracle.count_all(n, fixed_first_row=True)
+
+
+# ------------------------------------------------------------------ config 2
+
+@pytest.mark.parametrize("extra", [0, 3])
+def test_config2_dls7_first_row(extra):
+    n = 7
+    d = D.default_split_depth(n) + extra
+    recs = D.dls_split(n, d)
+    counts, total, nodes = _gpu(n, False, recs, d)
+    want, want_nodes = _oracle_per_prefix(n, False, recs, d)
+    assert (counts == want).all()
+    assert nodes == want_nodes
+    assert total == oracle.count_all(n)
+    r = D.count_squares(n)
+    assert r["count"] == total and r["total_all_first_rows"] == math.factorial(7) * total
+
+
+# ------------------------------------------------------------------ config 3
+
+def test_config3_dls8_full_count_matches_paper():
+    r = D.count_squares(8)
+    assert r["n_prefix"] == 547896
+    assert r["count"] == paper_counts()["dls8_first_row_fixed"]
+    assert r["total_all_first_rows"] == math.factorial(8) * 7447587840
+
+
+def test_config3_dls8_sampled_prefixes():
+    n, d = 8, D.default_split_depth(8)
+    recs = D.dls_split(n, d)
+    counts, total, _ = _gpu(n, False, recs, d)
+    assert total == paper_counts()["dls8_first_row_fixed"]
+    rng = np.random.default_rng(8)
+    idx = np.concatenate([rng.choice(len(recs), 150, replace=False), [0, len(recs) - 1]])
+    want, _ = _oracle_per_prefix(n, False, recs[idx], d)
+    assert (counts[idx] == want).all()
+
+
+# ------------------------------------------------------------------ config 4
+
+def test_config4_vs8_full():
+    n, vs = 8, True
+    d = D.default_split_depth(n, vs)
+    recs = D.dls_split(n, d, vs)
+    counts, total, nodes = _gpu(n, vs, recs, d)
+    want, want_nodes = _oracle_per_prefix(n, vs, recs, d)
+    assert (counts == want).all()
+    assert nodes == want_nodes
+    assert total == oracle.count_all(n, vs=True)
+
+
+def _read_golden(name):
+    rows = {}
+    for line in open(golden(name)):
+        if line.startswith("#") or not line.strip():
+            continue
+        i, c, nd = line.split()[:3]
+        rows[int(i)] = (int(c), int(nd))
+    return rows
+
+
+def test_config4_vs10_seeded_prefixes():
+    n, vs = 10, True
+    recs = synth.diagonal_prefixes(synth.SEED_VS10, n, synth.N_VS10, vs=True)
+    d = D.default_split_depth(n, vs)
+    counts, total, _ = _gpu(n, vs, recs, d)
+    gold = _read_golden("vs10_prefix_counts.txt")
+    for i, (c, _) in gold.items():
+        assert int(counts[i]) == c, i
+    # property at any size: a prefix's count is the sum over its children
+    sub = recs[[0, 4095]]
+    c2, t2, _ = _gpu(n, vs, sub, d)
+    assert (c2 == counts[[0, 4095]]).all()
+
+
+def test_config4_vs10_children_vs_oracle():
+    """Deepen two seeded VS10 prefixes by two rows with the oracle's own prefix
+    enumeration; GPU counts of sampled children must equal the oracle's."""
+    n, vs = 10, True
+    recs = synth.diagonal_prefixes(synth.SEED_VS10, n, 3, vs=True)
+    d = D.default_split_depth(n, vs)
+    order = oracle.plan(n, vs)
+    extra = 8
+    rng = np.random.default_rng(10)
+    for r in recs[:2]:
+        kids = oracle.prefixes(n, vs, synth.to_int_grid(r), order[d:], extra)
+        pick = rng.choice(len(kids), min(12, len(kids)), replace=False)
+        kid_recs = np.where(kids[pick] < 0, 255, kids[pick]).astype(np.uint8)
+        counts, _, nodes = _gpu(n, vs, kid_recs, d + extra)
+        want, want_nodes = _oracle_per_prefix(n, vs, kid_recs, d + extra)
+        assert (counts == want).all()
+        assert nodes == want_nodes
+
+
+# ------------------------------------------------------------------ config 5
+
+def test_config5_dls9_seeded_prefixes():
+    n = 9
+    recs = synth.diagonal_prefixes(synth.SEED_DLS9, n, synth.N_DLS9)
+    d = D.default_split_depth(n)
+    counts, total, _ = _gpu(n, False, recs, d)
+    gold = _read_golden("dls9_prefix_counts.txt")
+    for i, (c, _) in gold.items():
+        assert int(counts[i]) == c, i
+
+
+def test_config5_dls9_children_vs_oracle():
+    n = 9
+    recs = synth.diagonal_prefixes(synth.SEED_DLS9, n, 2)
+    d = D.default_split_depth(n)
+    order = oracle.plan(n)
+    extra = 9
+    rng = np.random.default_rng(9)
+    for r in recs:
+        kids = oracle.prefixes(n, False, synth.to_int_grid(r), order[d:], extra)
+        pick = rng.choice(len(kids), min(10, len(kids)), replace=False)
+        kid_recs = np.where(kids[pick] < 0, 255, kids[pick]).astype(np.uint8)
+        counts, _, nodes = _gpu(n, False, kid_recs, d + extra)
+        want, want_nodes = _oracle_per_prefix(n, False, kid_recs, d + extra)
+        assert (counts == want).all()
+        assert nodes == want_nodes
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_small_orders(n):
+    r = D.count_squares(n)
+    assert r["count"] == oracle.count_all(n)
+    r = D.count_squares(n, fixed_first_row=False)
+    assert r["count"] == oracle.count_all(n, fixed_first_row=False)
+
+
+def test_empty_input():
+    recs = np.zeros((0, 8, 8), np.uint8)
+    counts, total, nodes = D.count_prefixes(8, recs)
+    assert total == 0 and nodes == 0 and counts.shape == (0,)
+
+
+@pytest.mark.parametrize("back", [0, 1, 2, 5])
+def test_deep_prefixes_ragged_tail(back):
+    # L = levels left for the kernel: 0 (records are complete squares), 1, 2, 5
+    n = 6
+    steps = len(D.dls_plan(n)[0])
+    d = steps - back
+    recs = D.dls_split(n, d)
+    counts, total, nodes = _gpu(n, False, recs, d)
+    want, want_nodes = _oracle_per_prefix(n, False, recs, d)
+    assert (counts == want).all() and nodes == want_nodes
+    assert total == oracle.count_all(n)
+
+
+def test_ragged_prefix_counts_not_multiple_of_warp():
+    n = 7
+    d = D.default_split_depth(n)
+    recs = D.dls_split(n, d)[:1001]
+    counts, total, _ = _gpu(n, False, recs, d)
+    want, _ = _oracle_per_prefix(n, False, recs, d)
+    assert (counts == want).all()
+
+
+def test_inconsistent_prefix_is_reported():
+    n = 7
+    d = D.default_split_depth(n)
+    recs = D.dls_split(n, d)[:64].copy()
+    recs[5, 1, 1] = recs[5, 0, 1]     # value repeated in column 1
+    with pytest.raises(D.DlsError) as e:
+        D.count_prefixes(n, recs, depth=d)
+    assert e.value.code == B.DLS_E_PREFIX
+
+
+def test_depth_below_diagonals_rejected():
+    n = 8
+    recs = D.dls_split(n, 5)
+    with pytest.raises(D.DlsError) as e:
+        D.dls_count(n, 5, recs)
+    assert e.value.code == B.DLS_E_ARG
+
+
+def test_device_buffers_and_async_stats():
+    import torch
+    n = 7
+    d = D.default_split_depth(n)
+    recs = D.dls_split(n, d)
+    dev = torch.from_numpy(recs).cuda()
+    out = torch.zeros(len(recs), dtype=torch.int64, device="cuda")
+    stats = torch.zeros(B.DLS_STATS_WORDS, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    D.dls_count_async(n, d, dev, out, stats, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    want = oracle.count_all(n)
+    assert int(stats[0]) == want and int(out.sum()) == want and int(stats[2]) == 0
+    total, _ = D.dls_count(n, d, dev, out_counts=out, stream=s.cuda_stream)
+    assert total == want and int(out.sum()) == want
+
+
+def test_repeatable():
+    n = 8
+    d = D.default_split_depth(n)
+    recs = D.dls_split(n, d)[:20000]
+    a = _gpu(n, False, recs, d)
+    b = _gpu(n, False, recs, d)
+    assert (a[0] == b[0]).all() and a[1:] == b[1:]

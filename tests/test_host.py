@@ -1,0 +1,123 @@
+"""Host-side product logic (CPU only): the C ABI loads and exports what the header
+declares; the Section 2.3 planner and the prefix splitter (both host C++ in
+libdls_b200.so) agree with the oracle; the GPU entry points refuse to run
+without a device (no CPU fallback)."""
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+import paper_1709_02599_b200 as D
+from paper_1709_02599_b200 import _binding as B
+from conftest import ROOT, golden
+from test_oracle import fig1
+
+
+def header_functions():
+    src = open(ROOT + "/include/dls_b200.h").read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z0-9_]+\s*\*?\s*(dls_[a-z_]+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = D.load()
+    names = header_functions()
+    assert set(names) >= {"dls_plan", "dls_split", "dls_count", "dls_count_async"}
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(B.EXPORTS)
+    assert "sm_100a" in D.dls_version()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", D.lib_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+@pytest.mark.parametrize("n", range(1, 11))
+@pytest.mark.parametrize("vs", [False, True])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_plan_matches_oracle(n, vs, fixed):
+    if vs and n % 2:
+        with pytest.raises(D.DlsError):
+            D.dls_plan(n, vs, fixed)
+        return
+    cells, forced, dd = D.dls_plan(n, vs, fixed)
+    pre = np.zeros((n, n), np.int32)
+    if fixed:
+        pre[0, :] = 1
+    assert cells.tolist() == oracle.plan(n, vs, pre)
+    # diag depth: the first prefix covering both diagonals
+    diag = {i * n + j for i in range(n) for j in range(n) if (i == j or i + j == n - 1) and not pre[i, j]}
+    covered = set()
+    for c in cells[:dd]:
+        i, j = divmod(int(c), n)
+        covered |= {i * n + j, i * n + (n - 1 - j)} if vs else {i * n + j}
+    assert diag <= covered
+    if dd:
+        i, j = divmod(int(cells[dd - 1]), n)
+        last = {i * n + j, i * n + (n - 1 - j)} if vs else {i * n + j}
+        assert last & diag
+
+
+def test_plan_fig1_and_forced_flags():
+    cells, forced, dd = D.dls_plan(9)
+    got = np.zeros((9, 9), int)
+    for s, c in enumerate(cells):
+        got[c // 9, c % 9] = s + 1
+    assert (got[1:] == fig1()).all()
+    assert dd == 15
+    # Fig. 1 step 13 (cell (8,0)) and step 15 (cell (8,8)) complete the antidiagonal
+    # and the main diagonal
+    assert forced[12] == 1 and forced[14] == 1 and forced[0] == 0
+
+
+@pytest.mark.parametrize("n,vs,fixed,depth", [
+    (4, False, True, 3), (5, False, True, 6), (6, False, True, 8), (6, False, False, 14),
+    (7, False, True, 12), (8, False, True, 9), (4, True, True, 3), (6, True, True, 5),
+    (8, True, True, 9), (10, True, True, 6), (9, False, True, 10)])
+def test_split_equals_oracle_prefixes(n, vs, fixed, depth):
+    got = D.dls_split(n, depth, vs, fixed)
+    g = oracle.first_row_grid(n) if fixed else oracle.empty_grid(n)
+    pre = np.zeros((n, n), np.int32)
+    if fixed:
+        pre[0, :] = 1
+    want = oracle.prefixes(n, vs, g, oracle.plan(n, vs, pre), depth)
+    # same records in the same (depth-first, increasing value) order
+    assert got.shape[0] == want.shape[0]
+    assert (synth.to_int_grid(got) == want).all()
+
+
+def test_split_sizes_and_edges():
+    assert D.dls_split(8, 14).shape == (547896, 8, 8)   # N=8 diagonal workunits
+    assert D.dls_split(2, 2).shape[0] == 0               # no DLS of order 2
+    assert D.dls_split(1, 0).shape == (1, 1, 1)
+    assert D.dls_split(5, 0).shape == (1, 5, 5)
+    with pytest.raises(D.DlsError):
+        D.dls_split(8, 99)
+    with pytest.raises(D.DlsError):
+        D.dls_split(11, 1)
+    with pytest.raises(D.DlsError):
+        D.dls_split(7, 1, symmetric=True)
+
+
+def test_dls9_decomposition_workunits():
+    """P:481 decomposes N=9 by the first 10 Fig. 1 cells.  The paper prints
+    1 225 884; the oracle (scripts/make_golden.py) finds 1 255 884 (reading R8)."""
+    want = int(open(golden("dls9_k10_workunits.txt")).read().split("\n")[-2])
+    lib = D.load()
+    assert lib.dls_split(9, 0, 1, 10, None, 0) == want
+
+
+def test_count_refuses_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    pre = D.dls_split(6, 8)
+    with pytest.raises(D.DlsError) as e:
+        D.dls_count(6, 8, pre)
+    assert e.value.code == B.DLS_E_NODEVICE
