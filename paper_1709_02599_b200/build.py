@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     tmp = LIB + ".tmp%d" % os.getpid()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "--cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+           "--cudart", "static", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -11,19 +11,22 @@
 //
 // How ("Kernel"):
 //  * persistent grid, one DFS per lane; the nested loops become one iterative
-//    step (descend / backtrack selected branch-free), so all busy lanes of a warp
-//    execute the same instruction stream;
-//  * per-level candidate sets L[] (Alg. 4's L[i][j]) live in a per-lane stack in
+//    step, chosen branch-free among  descend  (take the lowest candidate of the
+//    current cell),  advance  (unmark the value of the previous cell and
+//    mark its next candidate in ONE toggle: Alg. 4's "L &= L-1" then "LS = L & -L")
+//    and  backtrack; all busy lanes of a warp execute the same instructions;
+//  * per-level candidate sets (Alg. 4's L[i][j]) live in a per-lane stack in
 //    shared memory, u32 per level, layout [level][lane] (bank-conflict free);
-//    the "current" L is kept in a register, and its lowest set bit is the value
-//    assigned at that level, exactly as Alg. 4 keeps LS = L & -L;
-//  * Rows/Columns occupancy sets are packed bit fields in 64-bit registers, so a
-//    cell's candidate set is two funnel shifts and one LOP3;
-//  * a global atomic work queue hands prefixes to lanes (warp-aggregated: one
-//    atomic per warp refill); once it is drained, idle lanes receive the
-//    untried siblings of the shallowest open level of a busy lane of their warp
-//    (warp-vote donation, ballot/shuffle pairing);
-//  * counts: 32-bit per K-step burst -> 64-bit per lane -> atomicAdd per prefix
+//    the lowest set bit of a stacked L is the value assigned at that level;
+//  * Rows/Columns occupancy sets are bit fields in registers.  N <= 8: byte fields
+//    in 32-bit words -- a cell's candidates are two PRMT byte-selects and one LOP3,
+//    marks/unmarks are IMADs with per-cell power-of-two multipliers (FMA pipe,
+//    leaving the ALU pipe to the control flow).  N = 9, 10: 64-bit words with
+//    funnel shifts.  Per-transition geometry comes pre-decoded from a table;
+//  * a global atomic work queue hands prefixes to lanes (one atomic per warp
+//    refill); once it is drained, idle lanes receive the untried siblings of the
+//    shallowest open level of a busy lane of their warp (warp-vote donation);
+//  * counts: 32-bit per burst -> 64-bit per lane -> atomicAdd per prefix
 //    (optional) and one 64-bit atomicAdd per block for the total.
 #include <cuda_runtime.h>
 
@@ -39,90 +42,137 @@ namespace {
 typedef unsigned long long u64;
 
 constexpr int kMaxLevels = 100;     // n*n for n = 10
-constexpr int kBlock = 256;         // threads per CTA
 constexpr int kBurst = 32;          // DFS steps between warp scheduling points
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// One transition t (t = -1 .. L): "toggle a value at cell(t), then read the
+// candidates of cell(t+1)".  Eight words; the meaning depends on the mask layout.
+struct Tab {
+    uint32_t w[8];
+};
+
 struct Params {
     const uint8_t *prefixes;
     long long n_prefix;
-    u64 *counts;       // per-prefix counts (may be null)
+    u64 *counts;             // per-prefix counts (may be null)
     const uint32_t *parent;  // record -> output slot (null = identity; set by refinement)
-    u64 *stats;        // DLS_STATS_WORDS words, see dls_b200.h
-    u64 pat[2];        // cells assigned in a prefix, bit i*n+j
-    int L;             // number of searched levels (plan cells after the prefix)
-    int donate;        // enable warp-level subtree donation
-    uint32_t tab[kMaxLevels + 2];  // tab[l], l = 1..L: packed geometry of level l
+    u64 *stats;              // DLS_STATS_WORDS words, see dls_b200.h
+    u64 pat[2];              // cells assigned in a prefix, bit i*n+j
+    int L;                   // number of searched levels (plan cells after the prefix)
+    int donate;              // enable warp-level subtree donation
+    Tab tab[kMaxLevels + 2]; // tab[t + 1], t = -1 .. L
 };
 
-// ---------------------------------------------------------------- geometry
+// ---------------------------------------------------------------- mask layouts
 
-// Row / column sets are bit fields inside W 64-bit words.  For DLS a row field
-// holds the N value bits; for vertical symmetry a row field holds N/2 "pair"
-// bits (a row always contains v and N-1-v together) and only the N/2 left
-// columns are tracked (the right column N-1-j is the mirror of column j).
+// Row sets: for DLS the N value bits of a row; for vertical symmetry N/2 "pair"
+// bits (a row always holds v and N-1-v together), and only the N/2 left columns
+// are tracked (column N-1-j is the mirror of column j).
 template <int N, bool VS>
 struct Geo {
     static constexpr int H = N / 2;
-    static constexpr int RF = VS ? (H > 0 ? H : 1) : N;        // row field width
-    static constexpr int CF = N;                               // column field width
     static constexpr int NC = VS ? H : N;                      // tracked columns
+    static constexpr uint32_t ALLN = (1u << N) - 1u;
+    static constexpr uint32_t HMASK = (1u << H) - 1u;
+    static constexpr bool BYTES = N <= 8;                      // byte-field layout
+    static constexpr int RF = VS ? (H > 0 ? H : 1) : N;        // shift layout: row field width
+    static constexpr int CF = N;                               //               col field width
     static constexpr int RPW = 64 / RF;
     static constexpr int CPW = 64 / CF;
     static constexpr int WR = (N + RPW - 1) / RPW;
     static constexpr int WC = (NC + CPW - 1) / CPW;
-    static constexpr uint32_t ALLN = (1u << N) - 1u;
-    static constexpr uint32_t HMASK = (1u << H) - 1u;
-    // value v -> bit position used inside the kernel.  DLS: v.  VS: the mirror
-    // of position p is p +- H, so that a row's pair mask expands with one IMAD.
+    // value v -> bit position inside the kernel.  DLS: v.  VS: the mirror of
+    // position p is p +- H, so a row's pair mask expands with one IMAD.
     __host__ __device__ static constexpr int pos(int v) {
         return !VS ? v : (v < H ? v : H + (N - 1 - v));
     }
+    // value bit -> row-field bit
+    __device__ __forceinline__ static uint32_t rowbit(uint32_t b) {
+        return VS ? ((b | (b >> H)) & HMASK) : b;
+    }
+    __device__ __forceinline__ static uint32_t expand_row(uint32_t r) {
+        return VS ? (r & HMASK) * ((1u << H) + 1u) : r;
+    }
 };
 
-// tab entry: bits 0-5 row shift, bit 6 row word, bits 8-13 col shift, bit 14 col word
-__host__ __device__ inline uint32_t rsh(uint32_t e) { return e & 63u; }
-__host__ __device__ inline uint32_t rwd(uint32_t e) { return (e >> 6) & 1u; }
-__host__ __device__ inline uint32_t csh(uint32_t e) { return (e >> 8) & 63u; }
-__host__ __device__ inline uint32_t cwd(uint32_t e) { return (e >> 14) & 1u; }
+template <int N, bool VS, bool BYTES = Geo<N, VS>::BYTES>
+struct Masks;
 
-template <int W>
-__device__ __forceinline__ uint32_t field(const u64 (&a)[W], uint32_t sh, uint32_t wd) {
-    u64 w = a[0];
-    if (W == 2) w = wd ? a[W - 1] : a[0];
-    return (uint32_t)(w >> sh);
-}
-
-template <int W>
-__device__ __forceinline__ void flip(u64 (&a)[W], uint32_t sh, uint32_t wd, uint32_t bits) {
-    const u64 t = (u64)bits << sh;
-    if (W == 1) {
-        a[0] ^= t;
-    } else {
-        a[0] ^= wd ? 0ull : t;
-        a[W - 1] ^= wd ? t : 0ull;
-    }
-}
-
+// N <= 8: row r is byte r&3 of R[r>>2], column c is byte c&3 of C[c>>2].
+// Tab: w0..w3 = multipliers of cell(t)'s row/col byte in R0,R1,C0,C1
+//      (1 << 8*(r&3) in the word holding the field, 0 in the other);
+//      w4, w5 = PRMT selectors (row, col byte index 0..7) of cell(t+1).
 template <int N, bool VS>
-struct Lane {
+struct Masks<N, VS, true> {
+    typedef Geo<N, VS> G;
+    uint32_t R0, R1, C0, C1;
+
+    __device__ __forceinline__ void clear() { R0 = R1 = C0 = C1 = 0; }
+    __device__ __forceinline__ void set_row(int r, uint32_t m) { if (r < 4) R0 |= m << (8 * r); else R1 |= m << (8 * (r - 4)); }
+    __device__ __forceinline__ void set_col(int c, uint32_t m) { if (c < 4) C0 |= m << (8 * c); else C1 |= m << (8 * (c - 4)); }
+    // assign value bit bnew and remove value bit bold at the flip cell (either may be 0)
+    __device__ __forceinline__ void toggle(const uint4 &f, uint32_t bnew, uint32_t bold) {
+        const uint32_t dc = bnew - bold;                         // field changes by +bnew -bold
+        const uint32_t dr = VS ? G::rowbit(bnew) - G::rowbit(bold) : dc;
+        R0 += dr * f.x;
+        R1 += dr * f.y;
+        C0 += dc * f.z;
+        C1 += dc * f.w;
+    }
+    __device__ __forceinline__ uint32_t cand(const uint2 &c) const {
+        const uint32_t r = G::expand_row(__byte_perm(R0, R1, c.x));
+        const uint32_t k = __byte_perm(C0, C1, c.y);
+        return G::ALLN & ~(r | k);                               // AllN ^ (Rows | Columns)
+    }
+    typedef uint2 CT;
+};
+
+// N = 9, 10: row/column fields packed in 64-bit words (W of them), moved by
+// funnel shifts.  Tab: w0..w3 = row shift, row word, col shift, col word of
+// cell(t); w4..w7 = the same of cell(t+1).
+template <int N, bool VS>
+struct Masks<N, VS, false> {
     typedef Geo<N, VS> G;
     u64 R[G::WR];
     u64 C[G::WC];
 
-    __device__ __forceinline__ uint32_t cand(uint32_t e) const {
-        uint32_t r = field<G::WR>(R, rsh(e), rwd(e));
-        const uint32_t c = field<G::WC>(C, csh(e), cwd(e));
-        if (VS) r = (r & G::HMASK) * ((1u << G::H) + 1u);   // pairs -> both values
-        return G::ALLN & ~(r | c);
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int w = 0; w < G::WR; ++w) R[w] = 0;
+#pragma unroll
+        for (int w = 0; w < G::WC; ++w) C[w] = 0;
     }
-    __device__ __forceinline__ void toggle(uint32_t e, uint32_t b) {
-        uint32_t rb = b;
-        if (VS) rb = (b | (b >> G::H)) & G::HMASK;            // value bit -> pair bit
-        flip<G::WR>(R, rsh(e), rwd(e), rb);
-        flip<G::WC>(C, csh(e), cwd(e), b);
+    __device__ __forceinline__ void set_row(int r, uint32_t m) { R[r / G::RPW] |= (u64)m << ((r % G::RPW) * G::RF); }
+    __device__ __forceinline__ void set_col(int c, uint32_t m) { C[c / G::CPW] |= (u64)m << ((c % G::CPW) * G::CF); }
+    template <int W>
+    __device__ __forceinline__ static void flip(u64 (&a)[W], uint32_t sh, uint32_t wd, uint32_t bits) {
+        const u64 t = (u64)bits << sh;
+        if (W == 1) {
+            a[0] ^= t;
+        } else {
+            a[0] ^= wd ? 0ull : t;
+            a[W - 1] ^= wd ? t : 0ull;
+        }
     }
+    template <int W>
+    __device__ __forceinline__ static uint32_t field(const u64 (&a)[W], uint32_t sh, uint32_t wd) {
+        u64 w = a[0];
+        if (W == 2) w = wd ? a[W - 1] : a[0];
+        return (uint32_t)(w >> sh);
+    }
+    __device__ __forceinline__ void toggle(const uint4 &f, uint32_t bnew, uint32_t bold) {
+        const uint32_t xc = bnew ^ bold;
+        const uint32_t xr = VS ? (G::rowbit(bnew) ^ G::rowbit(bold)) : xc;
+        flip<G::WR>(R, f.x, f.y, xr);
+        flip<G::WC>(C, f.z, f.w, xc);
+    }
+    __device__ __forceinline__ uint32_t cand(const uint4 &c) const {
+        const uint32_t r = G::expand_row(field<G::WR>(R, c.x, c.y));
+        const uint32_t k = field<G::WC>(C, c.z, c.w);
+        return G::ALLN & ~(r | k);
+    }
+    typedef uint4 CT;
 };
 
 __host__ __device__ inline bool pat_bit(const u64 *pat, int c) {
@@ -133,27 +183,31 @@ __host__ __device__ inline bool pat_bit(const u64 *pat, int c) {
 // pattern cells assigned, values < N, no repeated value in a row, column or
 // diagonal, and (VS) mirror consistency LS[i][N-1-j] = N-1-LS[i][j].
 template <int N, bool VS>
-__device__ bool load_prefix(const uint8_t *__restrict__ rec, const Params &p, Lane<N, VS> &st) {
+__device__ __noinline__ bool load_prefix(const uint8_t *__restrict__ rec, const u64 pat0, const u64 pat1,
+                                         Masks<N, VS> &st) {
     typedef Geo<N, VS> G;
-    uint32_t rm[N], cm[N], sr[N], sc[G::NC > 0 ? G::NC : 1];
+    const u64 pat[2] = {pat0, pat1};
+    uint32_t cm[N], sc[G::NC > 0 ? G::NC : 1];
     uint32_t md = 0, ad = 0;
     bool ok = true;
+    st.clear();
 #pragma unroll
-    for (int i = 0; i < N; ++i) { rm[i] = cm[i] = sr[i] = 0; }
+    for (int j = 0; j < N; ++j) cm[j] = 0;
 #pragma unroll
     for (int j = 0; j < G::NC; ++j) sc[j] = 0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
+        uint32_t rm = 0, sr = 0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             const uint32_t v = __ldg(rec + i * N + j);
             const bool assigned = v != DLS_EMPTY;
-            ok &= assigned == pat_bit(p.pat, i * N + j);
+            ok &= assigned == pat_bit(pat, i * N + j);
             if (assigned) {
                 ok &= v < (uint32_t)N;
                 const uint32_t b = 1u << (v & 31u);
-                ok &= !(rm[i] & b) && !(cm[j] & b);
-                rm[i] |= b;
+                ok &= !(rm & b) && !(cm[j] & b);
+                rm |= b;
                 cm[j] |= b;
                 if (i == j) { ok &= !(md & b); md |= b; }
                 if (i + j == N - 1) { ok &= !(ad & b); ad |= b; }
@@ -162,66 +216,72 @@ __device__ bool load_prefix(const uint8_t *__restrict__ rec, const Params &p, La
                     ok &= m == (uint32_t)(N - 1) - v;
                     const uint32_t pb = 1u << (G::pos((int)(v & 15u)) & 31);
                     if (2 * j < N - 1) {
-                        sr[i] |= (pb | (pb >> G::H)) & G::HMASK;
+                        sr |= G::rowbit(pb);
                         sc[j < G::NC ? j : 0] |= pb;
                     }
                 } else {
-                    sr[i] |= b;
+                    sr |= b;
                     sc[j < G::NC ? j : 0] |= b;
                 }
             }
         }
+        st.set_row(i, sr);
     }
 #pragma unroll
-    for (int w = 0; w < G::WR; ++w) st.R[w] = 0;
-#pragma unroll
-    for (int w = 0; w < G::WC; ++w) st.C[w] = 0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) st.R[i / G::RPW] |= (u64)sr[i] << ((i % G::RPW) * G::RF);
-#pragma unroll
-    for (int j = 0; j < G::NC; ++j) st.C[j / G::CPW] |= (u64)sc[j] << ((j % G::CPW) * G::CF);
+    for (int j = 0; j < G::NC; ++j) st.set_col(j, sc[j]);
     return ok;
 }
 
-template <int W>
 __device__ __forceinline__ u64 warp_sum(u64 v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
     return v;
 }
 
+// Shared memory of one CTA (one CTA per SM, nthreads = blockDim.x lanes):
+//   F [L+2][32] uint4      toggle part of transition t (u = t+1), one copy per
+//   C [L+2][32] CT         lane index: every lane reads its own copy, so lanes
+//                          at different levels never collide on a bank
+//   S [L+2][nthreads] u32  per-lane stack of Alg. 4's L sets, slot u = level+1
 template <int N, bool VS>
-__global__ void __launch_bounds__(kBlock, (Geo<N, VS>::WR + Geo<N, VS>::WC > 2) ? 3 : 4)
+__global__ void __launch_bounds__(Geo<N, VS>::BYTES ? 1024 : 512, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
-    typedef Geo<N, VS> G;
-    extern __shared__ uint32_t smem[];
+    typedef Masks<N, VS> M;
+    typedef typename M::CT CT;
+    extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
-    uint32_t *tab_s = smem;                        // L + 2 entries (padded to 4)
-    uint32_t *stack = smem + ((L + 2 + 3) & ~3);   // (L + 2) slots x kBlock lanes
+    const int nthreads = blockDim.x;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
+    uint4 *const F = reinterpret_cast<uint4 *>(smem);
+    CT *const C = reinterpret_cast<CT *>(F + (L + 2) * 32);
+    uint32_t *const stack = reinterpret_cast<uint32_t *>(C + (L + 2) * 32);
 
-    for (int l = tid; l < L + 2; l += kBlock) tab_s[l] = l <= L ? p.tab[l] : 0u;
-    // slots for levels -1 and 0 are read (idle lanes, backtrack from level 1) but
-    // never written: they stay 0
+    for (int k = tid; k < (L + 2) * 32; k += nthreads) {
+        const Tab &e = p.tab[k >> 5];
+        F[k] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
+        if (Geo<N, VS>::BYTES) reinterpret_cast<uint2 *>(C)[k] = make_uint2(e.w[4], e.w[5]);
+        else reinterpret_cast<uint4 *>(C)[k] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+    }
+    // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
+    // but never written: they stay 0
     stack[tid] = 0u;
-    stack[kBlock + tid] = 0u;
+    stack[nthreads + tid] = 0u;
     __syncthreads();
-    // S[(l + 1) * kBlock] is the slot of level l (l = -1 .. L)
+    // slot of level l (l = -1 .. L): S[(l + 1) * nthreads];  transition t: Fl[(t + 1) * 32]
     uint32_t *const S = stack + tid;
+    const uint4 *const Fl = F + 32 + lane;     // Fl[t * 32] = toggle part of transition t
+    const CT *const Cl = C + 32 + lane;
+    const int kBlock = nthreads;
 
-    Lane<N, VS> st;
-#pragma unroll
-    for (int w = 0; w < G::WR; ++w) st.R[w] = 0;
-#pragma unroll
-    for (int w = 0; w < G::WC; ++w) st.C[w] = 0;
+    M st;
+    st.clear();
     int lvl = 0;           // 0: idle / finished, 1..L: searching level lvl
     uint32_t cur = 0;      // untried candidates at level lvl
-    uint32_t ecur = tab_s[0];
     long long pid = -1;    // prefix being searched
     u64 cnt = 0;           // completions found for pid by this lane
-    u64 tot = 0, steps_dn = 0, donations = 0;
+    u64 tot = 0, nodes = 0, donations = 0;
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
@@ -245,7 +305,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     const u64 my = base + (u64)__popc(idle & lt_mask);
                     if (my < n_prefix) {
                         pid = (long long)my;
-                        const bool ok = load_prefix<N, VS>(p.prefixes + my * (u64)(N * N), p, st);
+                        const bool ok = load_prefix<N, VS>(p.prefixes + my * (u64)(N * N), p.pat[0], p.pat[1], st);
                         if (!ok) {
                             atomicOr(p.stats + 2, 1ull);
                             lvl = 0;
@@ -255,9 +315,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
                             lvl = 0;
                             cur = 0;
                         } else {
-                            lvl = 1;
-                            ecur = tab_s[1];
-                            const uint32_t c = st.cand(ecur);
+                            lvl = 1;   // enter level 1: candidates of cell(1) = transition 0
+                            const uint32_t c = st.cand(Cl[0]);
                             if (L == 1) { cnt += __popc(c); cur = 0; } else { cur = c; }
                         }
                     }
@@ -308,13 +367,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     }
                     if (recv) {
                         pid = d_pid;
-                        load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p, st);
+                        load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
                         for (int l = 1; l < d_split; ++l) {
                             const uint32_t s = S[(l + 1) * kBlock];
-                            st.toggle(tab_s[l], s & (0u - s));
+                            st.toggle(Fl[l * 32], s & (0u - s), 0u);
                         }
                         lvl = d_split;
-                        ecur = tab_s[d_split];
                         cur = d_rest;
                         cnt = 0;
                     }
@@ -323,44 +381,46 @@ dls_search_kernel(const __grid_constant__ Params p) {
         }
 
         // ------------------------------------------------ kBurst DFS steps
-        uint32_t cnt32 = 0, dn32 = 0;
-#pragma unroll 4
+        uint32_t cnt32 = 0, ent32 = 0;
+#pragma unroll 8
         for (int s = 0; s < kBurst; ++s) {
             const bool dn = cur != 0u;
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
-            const int nl = max(dn ? lvl + 1 : lvl - 1, 0);
-            const uint32_t en = tab_s[nl];
-            const uint32_t sp = S[lvl * kBlock];          // slot of level lvl-1
-            if (dn) S[(lvl + 1) * kBlock] = cur;           // push L of level lvl (b = lowest)
-            const uint32_t bb = sp & (0u - sp);           // value assigned at lvl-1
-            st.toggle(dn ? ecur : en, dn ? b : bb);        // mark b / unmark bb (Alg. 4 XOR)
-            const uint32_t c = st.cand(en);                // AllN ^ (Rows | Columns)
+            const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
+            uint32_t *const sl = S + lvl * kBlock;         // slot of level lvl-1
+            const uint32_t sp = *sl;                       // L of level lvl-1 (lowest = assigned)
+            const uint32_t bb = sp & (0u - sp);
+            const uint32_t sibs = sp ^ bb;                 // L &= L-1
+            const uint32_t sb = sibs & (0u - sibs);        // next value of level lvl-1
+            const bool adv = dn || sibs != 0u;
+            if (adv) sl[dn ? kBlock : 0] = dn ? cur : sibs;   // push / update level t
+            st.toggle(Fl[t * 32], dn ? b : sb, dn ? 0u : bb); // mark / unmark (Alg. 4)
+            const uint32_t c = st.cand(Cl[t * 32]);           // AllN ^ (Rows | Columns) of cell(t+1)
+            const int nl = max(t + (adv ? 1 : 0), 0);
             const bool leaf = nl == L;
-            const uint32_t pc = leaf ? (uint32_t)__popc(c) : 0u;
-            cnt32 += pc;
-            dn32 += dn ? 1u : 0u;
-            cur = dn ? (leaf ? 0u : c) : (sp ^ bb);       // L &= L-1 on the way back
+            cnt32 += (adv && leaf) ? (uint32_t)__popc(c) : 0u;
+            ent32 += adv ? 1u : 0u;
+            cur = (adv && !leaf) ? c : 0u;
             lvl = nl;
-            ecur = en;
         }
         cnt += cnt32;
-        steps_dn += dn32;
+        nodes += ent32;
     }
 
     // ------------------------------------------------ block reduction, 1 atomic per block
-    __shared__ u64 red[3][kBlock / 32];
-    tot = warp_sum<1>(tot);
-    steps_dn = warp_sum<1>(steps_dn);
-    donations = warp_sum<1>(donations);
+    __shared__ u64 red[3][32];
+    tot = warp_sum(tot);
+    nodes = warp_sum(nodes);
+    donations = warp_sum(donations);
     if (lane == 0) {
         red[0][tid >> 5] = tot;
-        red[1][tid >> 5] = steps_dn;
+        red[1][tid >> 5] = nodes;
         red[2][tid >> 5] = donations;
     }
     __syncthreads();
     if (tid == 0) {
         u64 a = 0, b = 0, c = 0;
-        for (int w = 0; w < kBlock / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
+        for (int w = 0; w < nthreads / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
         atomicAdd(p.stats + 0, a);
         atomicAdd(p.stats + 1, b);
         atomicAdd(p.stats + 4, c);
@@ -388,18 +448,47 @@ KernelFn pick_kernel(int n, bool vs) {
     }
 }
 
-// host mirror of Geo<> for building tab entries
-void field_geometry(int n, bool vs, int *rf, int *rpw, int *cf, int *cpw) {
-    const int h = n / 2;
-    *rf = vs ? (h > 0 ? h : 1) : n;
-    *cf = n;
-    *rpw = 64 / *rf;
-    *cpw = 64 / *cf;
-}
-
 int cuda_fail(cudaError_t e, const char *what) {
     dls::set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return DLS_E_CUDA;
+}
+
+// Host mirror of the device layouts: the per-transition table entries.
+void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
+    const int L = (int)level_cells.size();
+    const bool bytes = n <= 8;
+    const int h = n / 2;
+    const int rf = vs ? (h > 0 ? h : 1) : n, cf = n;
+    const int rpw = 64 / rf, cpw = 64 / cf;
+    auto cell_of = [&](int l) { return level_cells[l - 1]; };   // level l = 1..L
+    for (int t = -1; t <= L; ++t) {
+        Tab &e = tab[t + 1];
+        std::memset(&e, 0, sizeof(e));
+        if (t >= 1) {                       // toggle part: cell(t)
+            const int i = cell_of(t) / n, j = cell_of(t) % n;
+            if (bytes) {
+                (i < 4 ? e.w[0] : e.w[1]) = 1u << (8 * (i & 3));
+                (j < 4 ? e.w[2] : e.w[3]) = 1u << (8 * (j & 3));
+            } else {
+                e.w[0] = (uint32_t)((i % rpw) * rf);
+                e.w[1] = (uint32_t)(i / rpw);
+                e.w[2] = (uint32_t)((j % cpw) * cf);
+                e.w[3] = (uint32_t)(j / cpw);
+            }
+        }
+        if (t + 1 >= 1 && t + 1 <= L) {     // read part: cell(t+1)
+            const int i = cell_of(t + 1) / n, j = cell_of(t + 1) % n;
+            if (bytes) {
+                e.w[4] = (uint32_t)i;
+                e.w[5] = (uint32_t)j;
+            } else {
+                e.w[4] = (uint32_t)((i % rpw) * rf);
+                e.w[5] = (uint32_t)(i / rpw);
+                e.w[6] = (uint32_t)((j % cpw) * cf);
+                e.w[7] = (uint32_t)(j / cpw);
+            }
+        }
+    }
 }
 
 // Everything a launch needs that depends only on (n, vs, fixed_first_row, depth).
@@ -416,15 +505,8 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
     }
     std::memset(prm, 0, sizeof(*prm));
     prm->L = steps - depth;
-    int rf, rpw, cf, cpw;
-    field_geometry(n, symmetric, &rf, &rpw, &cf, &cpw);
-    for (int l = 1; l <= prm->L; ++l) {
-        const int cell = plan.cells[depth + l - 1];
-        const int i = cell / n, j = cell % n;
-        const uint32_t e = (uint32_t)((i % rpw) * rf) | ((uint32_t)(i / rpw) << 6) |
-                           ((uint32_t)((j % cpw) * cf) << 8) | ((uint32_t)(j / cpw) << 14);
-        prm->tab[l] = e;
-    }
+    std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.end());
+    fill_tab(n, symmetric, level_cells, prm->tab);
     // assigned-cell pattern of a depth-`depth` prefix
     auto set = [&](int c) { prm->pat[c >> 6] |= 1ull << (c & 63); };
     if (fixed_first_row)
@@ -438,23 +520,33 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
     return DLS_OK;
 }
 
+size_t smem_bytes(int n, bool vs, int L, int nthreads) {
+    const size_t ct = n <= 8 ? 8 : 16;
+    return (size_t)(L + 2) * 32 * (16 + ct) + (size_t)(L + 2) * nthreads * sizeof(uint32_t);
+}
+
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     KernelFn fn = pick_kernel(n, vs);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
-    const size_t smem = (size_t)(((prm.L + 2 + 3) & ~3) + (prm.L + 2) * kBlock) * sizeof(uint32_t);
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e;
+    int dev = 0, sms = 0, smem_max = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
         return cuda_fail(e, "cudaDeviceGetAttribute");
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)fn, kBlock, smem)) != cudaSuccess)
-        return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (per_sm < 1) { dls::set_error("kernel does not fit on an SM"); return DLS_E_CUDA; }
-    long long want_blocks = (long long)sms * per_sm;
-    const long long need = (prm.n_prefix + kBlock - 1) / kBlock;  // no more CTAs than work
-    if (need < want_blocks) want_blocks = need > 0 ? need : 1;
-    fn<<<(unsigned)want_blocks, kBlock, smem, stream>>>(prm);
+    if ((e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+        return cuda_fail(e, "cudaDeviceGetAttribute");
+    smem_max -= 1024;   // static shared memory of the kernel
+    // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
+    int nthreads = n <= 8 ? 1024 : 512;   // = the kernel's __launch_bounds__
+    while (nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
+    const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
+    if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
+    if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return cuda_fail(e, "cudaFuncSetAttribute");
+    long long blocks = sms;
+    const long long need = (prm.n_prefix + nthreads - 1) / nthreads;  // no more CTAs than work
+    if (need < blocks) blocks = need > 0 ? need : 1;
+    fn<<<(unsigned)blocks, nthreads, smem, stream>>>(prm);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "kernel launch");
     return DLS_OK;
 }
