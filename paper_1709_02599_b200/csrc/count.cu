@@ -102,30 +102,45 @@ struct Masks;
 // N <= 8: row r is byte r&3 of R[r>>2], column c is byte c&3 of C[c>>2].
 // Tab: w0..w3 = multipliers of cell(t)'s row/col byte in R0,R1,C0,C1
 //      (1 << 8*(r&3) in the word holding the field, 0 in the other);
-//      w4, w5 = PRMT selectors (row, col byte index 0..7) of cell(t+1).
+//      w4, w5 = PRMT selectors (row, col byte index 0..7) of cell(t+1); bit 16 of
+//      w4 = "cell(t+1) is the last level" (leaf), bit 16 of w5 = not leaf (PRMT
+//      reads only bits 0..15 of its selector).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
 template <int N, bool VS>
 struct Masks<N, VS, true> {
     typedef Geo<N, VS> G;
+    typedef uint2 CT;
     uint32_t R0, R1, C0, C1;
 
     __device__ __forceinline__ void clear() { R0 = R1 = C0 = C1 = 0; }
     __device__ __forceinline__ void set_row(int r, uint32_t m) { if (r < 4) R0 |= m << (8 * r); else R1 |= m << (8 * (r - 4)); }
     __device__ __forceinline__ void set_col(int c, uint32_t m) { if (c < 4) C0 |= m << (8 * c); else C1 |= m << (8 * (c - 4)); }
-    // assign value bit bnew and remove value bit bold at the flip cell (either may be 0)
+    // fields change by +bnew -bold (bnew absent, bold present: no carries between fields)
     __device__ __forceinline__ void toggle(const uint4 &f, uint32_t bnew, uint32_t bold) {
-        const uint32_t dc = bnew - bold;                         // field changes by +bnew -bold
+        const uint32_t dc = bnew - bold;
         const uint32_t dr = VS ? G::rowbit(bnew) - G::rowbit(bold) : dc;
-        R0 += dr * f.x;
+        toggle_d(f, dr, dc);
+    }
+    __device__ __forceinline__ void toggle_d(const uint4 &f, uint32_t dr, uint32_t dc) {
+        R0 += dr * f.x;      // IMAD: mark/unmark on the FMA pipe
         R1 += dr * f.y;
         C0 += dc * f.z;
         C1 += dc * f.w;
     }
     __device__ __forceinline__ uint32_t cand(const uint2 &c) const {
-        const uint32_t r = G::expand_row(__byte_perm(R0, R1, c.x));
-        const uint32_t k = __byte_perm(C0, C1, c.y);
+        const uint32_t r = G::expand_row(prmt(R0, R1, c.x));
+        const uint32_t k = prmt(C0, C1, c.y);
         return G::ALLN & ~(r | k);                               // AllN ^ (Rows | Columns)
     }
-    typedef uint2 CT;
+    __device__ __forceinline__ static void leaf_flags(const uint2 &c, int, int, uint32_t &leaf, uint32_t &notleaf) {
+        leaf = __umulhi(c.x, 65536u);
+        notleaf = __umulhi(c.y, 65536u);
+    }
 };
 
 // N = 9, 10: row/column fields packed in 64-bit words (W of them), moved by
@@ -171,6 +186,10 @@ struct Masks<N, VS, false> {
         const uint32_t r = G::expand_row(field<G::WR>(R, c.x, c.y));
         const uint32_t k = field<G::WC>(C, c.z, c.w);
         return G::ALLN & ~(r | k);
+    }
+    __device__ __forceinline__ static void leaf_flags(const uint4 &, int nl, int L, uint32_t &leaf, uint32_t &notleaf) {
+        leaf = nl == L ? 1u : 0u;
+        notleaf = 1u - leaf;
     }
     typedef uint4 CT;
 };
@@ -238,42 +257,55 @@ __device__ __forceinline__ u64 warp_sum(u64 v) {
     return v;
 }
 
-// Shared memory of one CTA (one CTA per SM, nthreads = blockDim.x lanes):
-//   F [L+2][32] uint4      toggle part of transition t (u = t+1), one copy per
-//   C [L+2][32] CT         lane index: every lane reads its own copy, so lanes
-//                          at different levels never collide on a bank
-//   S [L+2][nthreads] u32  per-lane stack of Alg. 4's L sets, slot u = level+1
+// Shared memory of one CTA (one CTA per SM, NT lanes):
+//   per transition u = t+1 (t = -1 .. L) a block of 32 toggle entries (uint4)
+//   followed by 32 read entries (CT), one copy per lane index: every lane reads its
+//   own copy, so lanes at different levels never collide on a bank;
+//   then S [L+2][NT] u32, the per-lane stack of Alg. 4's L sets (slot = level+1).
+template <int N, bool VS>
+struct Layout {
+    static constexpr bool BYTES = Geo<N, VS>::BYTES;
+    static constexpr int NT_FIXED = BYTES ? 1024 : 0;        // lanes per CTA (0 = runtime)
+    static constexpr int CTW = BYTES ? 2 : 4;                 // words of a read entry
+    static constexpr int BLK_WORDS = 32 * (4 + CTW);          // words per transition block
+};
+
 template <int N, bool VS>
 __global__ void __launch_bounds__(Geo<N, VS>::BYTES ? 1024 : 512, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
+    typedef Layout<N, VS> LY;
     extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
-    const int nthreads = blockDim.x;
+    const int NT = LY::NT_FIXED ? LY::NT_FIXED : (int)blockDim.x;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    uint4 *const F = reinterpret_cast<uint4 *>(smem);
-    CT *const C = reinterpret_cast<CT *>(F + (L + 2) * 32);
-    uint32_t *const stack = reinterpret_cast<uint32_t *>(C + (L + 2) * 32);
+    uint32_t *const stack = smem + (L + 2) * LY::BLK_WORDS;
 
-    for (int k = tid; k < (L + 2) * 32; k += nthreads) {
+    for (int k = tid; k < (L + 2) * 32; k += NT) {
         const Tab &e = p.tab[k >> 5];
-        F[k] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
-        if (Geo<N, VS>::BYTES) reinterpret_cast<uint2 *>(C)[k] = make_uint2(e.w[4], e.w[5]);
-        else reinterpret_cast<uint4 *>(C)[k] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+        uint32_t *const blk = smem + (k >> 5) * LY::BLK_WORDS;
+        reinterpret_cast<uint4 *>(blk)[k & 31] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
+        if (LY::BYTES) reinterpret_cast<uint2 *>(blk + 128)[k & 31] = make_uint2(e.w[4], e.w[5]);
+        else reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
     stack[tid] = 0u;
-    stack[nthreads + tid] = 0u;
+    stack[NT + tid] = 0u;
     __syncthreads();
-    // slot of level l (l = -1 .. L): S[(l + 1) * nthreads];  transition t: Fl[(t + 1) * 32]
+    // slot of level l (l = -1 .. L): S[(l + 1) * NT]
     uint32_t *const S = stack + tid;
-    const uint4 *const Fl = F + 32 + lane;     // Fl[t * 32] = toggle part of transition t
-    const CT *const Cl = C + 32 + lane;
-    const int kBlock = nthreads;
+    // transition t: Fl[t * kBlk] (toggle part), Cl[t * kBlkC] (read part)
+    constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
+    constexpr int kBlkC = LY::BLK_WORDS / LY::CTW;           // block stride in CT units
+    const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + LY::BLK_WORDS) + lane;
+    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128) + lane;
+    const int kBlock = NT;
+    const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte views for t-offsets
+    const char *const Cb = reinterpret_cast<const char *>(Cl);
 
     M st;
     st.clear();
@@ -316,7 +348,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                             cur = 0;
                         } else {
                             lvl = 1;   // enter level 1: candidates of cell(1) = transition 0
-                            const uint32_t c = st.cand(Cl[0]);
+                            const uint32_t c = st.cand(Cl[0]);   // transition 0 reads cell(1)
                             if (L == 1) { cnt += __popc(c); cur = 0; } else { cur = c; }
                         }
                     }
@@ -370,7 +402,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
                         for (int l = 1; l < d_split; ++l) {
                             const uint32_t s = S[(l + 1) * kBlock];
-                            st.toggle(Fl[l * 32], s & (0u - s), 0u);
+                            st.toggle(Fl[l * kBlk], s & (0u - s), 0u);
                         }
                         lvl = d_split;
                         cur = d_rest;
@@ -384,23 +416,35 @@ dls_search_kernel(const __grid_constant__ Params p) {
         uint32_t cnt32 = 0, ent32 = 0;
 #pragma unroll 8
         for (int s = 0; s < kBurst; ++s) {
-            const bool dn = cur != 0u;
+            const bool dn = cur != 0u;                     // descend: cell(lvl) has candidates
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
             const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
-            uint32_t *const sl = S + lvl * kBlock;         // slot of level lvl-1
-            const uint32_t sp = *sl;                       // L of level lvl-1 (lowest = assigned)
+            uint32_t *const sl = S + lvl * NT;             // slot of level lvl-1
+            const uint32_t sp = *sl;                       // its L (lowest bit = assigned value)
             const uint32_t bb = sp & (0u - sp);
-            const uint32_t sibs = sp ^ bb;                 // L &= L-1
+            const uint32_t sibs = sp - bb;                 // L &= L-1
             const uint32_t sb = sibs & (0u - sibs);        // next value of level lvl-1
-            const bool adv = dn || sibs != 0u;
-            if (adv) sl[dn ? kBlock : 0] = dn ? cur : sibs;   // push / update level t
-            st.toggle(Fl[t * 32], dn ? b : sb, dn ? 0u : bb); // mark / unmark (Alg. 4)
-            const uint32_t c = st.cand(Cl[t * 32]);           // AllN ^ (Rows | Columns) of cell(t+1)
+            const bool mv = !dn && sibs != 0u;             // advance: re-assign level lvl-1
+            if (dn) sl[NT] = cur;                          // push L of level lvl
+            if (mv) sl[0] = sibs;
+            const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
+            const uint4 f = *reinterpret_cast<const uint4 *>(Fb + toff);
+            const CT cs = *reinterpret_cast<const CT *>(Cb + toff);
+            if constexpr (VS || !Geo<N, VS>::BYTES) {
+                st.toggle(f, dn ? b : sb, dn ? 0u : bb);                          // mark / unmark
+            } else {
+                const uint32_t d = dn ? b : sb - bb;                              // mark / unmark
+                st.toggle_d(f, d, d);
+            }
+            const uint32_t c = st.cand(cs);               // AllN ^ (Rows | Columns) of cell(t+1)
+            const bool adv = dn || mv;
+            const uint32_t c2 = adv ? c : 0u;
             const int nl = max(t + (adv ? 1 : 0), 0);
-            const bool leaf = nl == L;
-            cnt32 += (adv && leaf) ? (uint32_t)__popc(c) : 0u;
+            uint32_t leaf, notleaf;
+            M::leaf_flags(cs, nl, L, leaf, notleaf);
+            cnt32 += (uint32_t)__popc(c2) * leaf;          // complete squares at the last cell
             ent32 += adv ? 1u : 0u;
-            cur = (adv && !leaf) ? c : 0u;
+            cur = c2 * notleaf;
             lvl = nl;
         }
         cnt += cnt32;
@@ -420,7 +464,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     __syncthreads();
     if (tid == 0) {
         u64 a = 0, b = 0, c = 0;
-        for (int w = 0; w < nthreads / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
+        for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
         atomicAdd(p.stats + 0, a);
         atomicAdd(p.stats + 1, b);
         atomicAdd(p.stats + 4, c);
@@ -479,8 +523,9 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
         if (t + 1 >= 1 && t + 1 <= L) {     // read part: cell(t+1)
             const int i = cell_of(t + 1) / n, j = cell_of(t + 1) % n;
             if (bytes) {
-                e.w[4] = (uint32_t)i;
-                e.w[5] = (uint32_t)j;
+                const bool leaf = t + 1 == L;
+                e.w[4] = (uint32_t)i | (leaf ? 1u << 16 : 0u);
+                e.w[5] = (uint32_t)j | (leaf ? 0u : 1u << 16);
             } else {
                 e.w[4] = (uint32_t)((i % rpw) * rf);
                 e.w[5] = (uint32_t)(i / rpw);
@@ -537,8 +582,8 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
         return cuda_fail(e, "cudaDeviceGetAttribute");
     smem_max -= 1024;   // static shared memory of the kernel
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
-    int nthreads = n <= 8 ? 1024 : 512;   // = the kernel's __launch_bounds__
-    while (nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
+    int nthreads = n <= 8 ? 1024 : 512;   // = the kernel's __launch_bounds__ (byte layout: fixed)
+    while (n > 8 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
     const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
