@@ -32,6 +32,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -45,6 +46,16 @@ constexpr int kMaxLevels = 100;     // n*n for n = 10
 constexpr int kBurst = 32;          // DFS steps between warp scheduling points
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this
 constexpr unsigned kFull = 0xFFFFFFFFu;
+// Device-wide donation pool (global memory, one per launch): control words
+// [0] active warps, [1] waiting warps, [2] head (claimed), [3] tail (reserved),
+// then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1/w2 = pid,
+// w3 = split level | untried siblings << 16, w4.. = the values (bit indices) of
+// levels 1..split-1, 4 bits each.
+constexpr uint32_t kPoolSlots = 16384;
+constexpr uint32_t kPoolLimit = 8192;   // producers stop while this many are pending
+constexpr int kSlotWords = 32;
+constexpr int kPoolHeader = 32;
+constexpr size_t kPoolBytes = (size_t)(kPoolHeader + kPoolSlots * kSlotWords) * 4;
 
 // One transition t (t = -1 .. L): "toggle a value at cell(t), then read the
 // candidates of cell(t+1)".  Eight words; the meaning depends on the mask layout.
@@ -58,6 +69,7 @@ struct Params {
     u64 *counts;             // per-prefix counts (may be null)
     const uint32_t *parent;  // record -> output slot (null = identity; set by refinement)
     u64 *stats;              // DLS_STATS_WORDS words, see dls_b200.h
+    uint32_t *pool;          // device-wide donation pool (kPoolBytes, zeroed)
     u64 pat[2];              // cells assigned in a prefix, bit i*n+j
     int L;                   // number of searched levels (plan cells after the prefix)
     int donate;              // enable warp-level subtree donation
@@ -307,6 +319,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte views for t-offsets
     const char *const Cb = reinterpret_cast<const char *>(Cl);
 
+    uint32_t *const pool = p.pool;
+    if (lane == 0) atomicAdd(pool + 0, 1u);        // this warp is active
+    bool waiting = false;
+
     M st;
     st.clear();
     int lvl = 0;           // 0: idle / finished, 1..L: searching level lvl
@@ -314,6 +330,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     long long pid = -1;    // prefix being searched
     u64 cnt = 0;           // completions found for pid by this lane
     u64 tot = 0, nodes = 0, donations = 0;
+    uint32_t bursts = 0, busy_bursts = 0;   // lane utilisation (stats[5] / stats[6])
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
@@ -357,10 +374,63 @@ dls_search_kernel(const __grid_constant__ Params p) {
         }
         if (qempty) {
             const unsigned idle = __ballot_sync(kFull, pid < 0);
-            if (idle == kFull) break;
-            if (idle && p.donate) {
-                // ---- warp-vote donation: busy lanes with an open level give the
-                // untried siblings of their shallowest open level to idle lanes.
+            if (idle == kFull) {
+                // ---- whole warp idle: take subtrees other warps donated to the
+                // device-wide pool, or leave once no warp is active and none is pending
+                uint32_t got = 0, h0 = 0, done = 0;
+                if (lane == 0) {
+                    if (!waiting) {
+                        atomicAdd(pool + 1, 1u);
+                        __threadfence();
+                        atomicSub(pool + 0, 1u);
+                    }
+                    if (atomicAdd(pool + 3, 0u) != atomicAdd(pool + 2, 0u)) {
+                        atomicAdd(pool + 0, 1u);           // tentatively active before claiming
+                        for (int tries = 0; tries < 8 && !got; ++tries) {
+                            const uint32_t h = atomicAdd(pool + 2, 0u), t = atomicAdd(pool + 3, 0u);
+                            const int avail = (int)(t - h);
+                            if (avail <= 0) break;
+                            const uint32_t k = min(avail, 32);
+                            if (atomicCAS(pool + 2, h, h + k) == h) { got = k; h0 = h; }
+                        }
+                        if (got) atomicSub(pool + 1, 1u);
+                        else atomicSub(pool + 0, 1u);
+                    }
+                    if (!got) {
+                        const uint32_t a = atomicAdd(pool + 0, 0u);
+                        __threadfence();
+                        done = (a == 0u && atomicAdd(pool + 2, 0u) == atomicAdd(pool + 3, 0u)) ? 1u : 0u;
+                    }
+                }
+                got = __shfl_sync(kFull, got, 0);
+                h0 = __shfl_sync(kFull, h0, 0);
+                done = __shfl_sync(kFull, done, 0);
+                if (done) break;
+                waiting = got == 0;
+                if (!got) {
+                    __nanosleep(1000);
+                    continue;
+                }
+                if ((uint32_t)lane < got) {
+                    const uint32_t ticket = h0 + lane;
+                    const volatile uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
+                    while (slot[0] != ticket + 1u) __nanosleep(64);
+                    __threadfence();
+                    pid = (long long)((u64)slot[1] | ((u64)slot[2] << 32));
+                    const uint32_t w3 = slot[3];
+                    const int split = (int)(w3 & 0xFFFFu);
+                    for (int l = 1; l < split; ++l) {
+                        const uint32_t v = (slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u;
+                        S[(l + 1) * kBlock] = 1u << v;
+                    }
+                    load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
+                    for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * kBlock], 0u);
+                    lvl = split;
+                    cur = w3 >> 16;
+                    cnt = 0;
+                }
+            } else {
+                // shallowest open level of each busy lane (its untried siblings)
                 int split = 0;
                 uint32_t rest = 0;
                 if (pid >= 0 && lvl > 0) {
@@ -373,46 +443,84 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         rest = cur & (cur - 1u);   // keep the lowest for ourselves
                     }
                 }
-                const unsigned donors = __ballot_sync(kFull, split > 0);
-                const int pairs = min(__popc(donors), __popc(idle));
-                if (pairs) {
+                if (idle && p.donate) {
+                    // ---- warp-vote donation to the idle lanes of this warp:
                     // k-th idle lane <- k-th donor lane
-                    const int my_rank = __popc(idle & lt_mask);
-                    int src = 0;
-                    if (pid < 0 && my_rank < pairs) src = __fns(donors, 0, my_rank + 1);
-                    const int dn_rank = __popc(donors & lt_mask);
-                    const int d_split = __shfl_sync(kFull, split, src);
-                    const uint32_t d_rest = __shfl_sync(kFull, rest, src);
-                    const long long d_pid = __shfl_sync(kFull, pid, src);
-                    const bool recv = pid < 0 && my_rank < pairs;
-                    const bool give = split > 0 && dn_rank < pairs;
-                    if (recv) {
-                        // copy the donor's path above the split level
-                        uint32_t *const Sd = stack + (tid - lane + src);
-                        for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
-                    }
-                    __syncwarp();
-                    if (give) {
-                        if (split < lvl) S[(split + 1) * kBlock] &= 0u - S[(split + 1) * kBlock];
-                        else cur &= 0u - cur;
-                        ++donations;
-                    }
-                    if (recv) {
-                        pid = d_pid;
-                        load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
-                        for (int l = 1; l < d_split; ++l) {
-                            const uint32_t s = S[(l + 1) * kBlock];
-                            st.toggle(Fl[l * kBlk], s & (0u - s), 0u);
+                    const unsigned donors = __ballot_sync(kFull, split > 0);
+                    const int pairs = min(__popc(donors), __popc(idle));
+                    if (pairs) {
+                        const int my_rank = __popc(idle & lt_mask);
+                        int src = 0;
+                        if (pid < 0 && my_rank < pairs) src = __fns(donors, 0, my_rank + 1);
+                        const int dn_rank = __popc(donors & lt_mask);
+                        const int d_split = __shfl_sync(kFull, split, src);
+                        const uint32_t d_rest = __shfl_sync(kFull, rest, src);
+                        const long long d_pid = __shfl_sync(kFull, pid, src);
+                        const bool recv = pid < 0 && my_rank < pairs;
+                        const bool give = split > 0 && dn_rank < pairs;
+                        if (recv) {
+                            // copy the donor's path above the split level
+                            uint32_t *const Sd = stack + (tid - lane + src);
+                            for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
                         }
-                        lvl = d_split;
-                        cur = d_rest;
-                        cnt = 0;
+                        __syncwarp();
+                        if (give) {
+                            if (split < lvl) S[(split + 1) * kBlock] &= 0u - S[(split + 1) * kBlock];
+                            else cur &= 0u - cur;
+                            ++donations;
+                        }
+                        if (recv) {
+                            pid = d_pid;
+                            load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
+                            for (int l = 1; l < d_split; ++l) {
+                                const uint32_t s = S[(l + 1) * kBlock];
+                                st.toggle(Fl[l * kBlk], s & (0u - s), 0u);
+                            }
+                            lvl = d_split;
+                            cur = d_rest;
+                            cnt = 0;
+                        }
+                    }
+                } else if (p.donate) {
+                    // ---- no idle lane here: feed the device-wide pool if a warp waits
+                    uint32_t feed = 0;
+                    if (lane == 0) {
+                        const volatile uint32_t *vp = pool;
+                        feed = (vp[1] != 0u && (int)(vp[3] - vp[2]) < (int)kPoolLimit) ? 1u : 0u;
+                    }
+                    feed = __shfl_sync(kFull, feed, 0);
+                    if (feed) {
+                        // the lane with the shallowest open level donates it
+                        const uint32_t key = split > 0 ? ((uint32_t)split << 5) | (uint32_t)lane : 0xFFFFFFFFu;
+                        const uint32_t best = __reduce_min_sync(kFull, key);
+                        if (best != 0xFFFFFFFFu && (best & 31u) == (uint32_t)lane) {
+                            const uint32_t ticket = atomicAdd(pool + 3, 1u);
+                            uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
+                            slot[1] = (uint32_t)((u64)pid & 0xFFFFFFFFull);
+                            slot[2] = (uint32_t)((u64)pid >> 32);
+                            slot[3] = (uint32_t)split | (rest << 16);
+                            for (int w = 0; w < (split + 6) / 8; ++w) {
+                                uint32_t word = 0;
+                                for (int k = 0; k < 8; ++k) {
+                                    const int l = 1 + w * 8 + k;
+                                    if (l < split) word |= (uint32_t)(__ffs(S[(l + 1) * kBlock]) - 1) << (4 * k);
+                                }
+                                slot[4 + w] = word;
+                            }
+                            __threadfence();
+                            *(volatile uint32_t *)slot = ticket + 1u;
+                            if (split < lvl) S[(split + 1) * kBlock] &= 0u - S[(split + 1) * kBlock];
+                            else cur &= 0u - cur;
+                            ++donations;
+                        }
                     }
                 }
             }
         }
 
         // ------------------------------------------------ kBurst DFS steps
+        ++bursts;
+        busy_bursts += pid >= 0 ? 1u : 0u;
         uint32_t cnt32 = 0, ent32 = 0;
 #pragma unroll 8
         for (int s = 0; s < kBurst; ++s) {
@@ -452,22 +560,24 @@ dls_search_kernel(const __grid_constant__ Params p) {
     }
 
     // ------------------------------------------------ block reduction, 1 atomic per block
-    __shared__ u64 red[3][32];
-    tot = warp_sum(tot);
-    nodes = warp_sum(nodes);
-    donations = warp_sum(donations);
+    __shared__ u64 red[5][32];
+    u64 v[5] = {tot, nodes, donations, busy_bursts, bursts};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = warp_sum(v[k]);
     if (lane == 0) {
-        red[0][tid >> 5] = tot;
-        red[1][tid >> 5] = nodes;
-        red[2][tid >> 5] = donations;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) red[k][tid >> 5] = v[k];
     }
     __syncthreads();
     if (tid == 0) {
-        u64 a = 0, b = 0, c = 0;
-        for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; c += red[2][w]; }
-        atomicAdd(p.stats + 0, a);
-        atomicAdd(p.stats + 1, b);
-        atomicAdd(p.stats + 4, c);
+        u64 a[5] = {0, 0, 0, 0, 0};
+        for (int w = 0; w < NT / 32; ++w)
+            for (int k = 0; k < 5; ++k) a[k] += red[k][w];
+        atomicAdd(p.stats + 0, a[0]);   // squares
+        atomicAdd(p.stats + 1, a[1]);   // nodes above the leaves
+        atomicAdd(p.stats + 4, a[2]);   // donations
+        atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
+        atomicAdd(p.stats + 6, a[4]);   // lane-bursts
     }
 }
 
@@ -588,11 +698,16 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute");
-    long long blocks = sms;
-    const long long need = (prm.n_prefix + nthreads - 1) / nthreads;  // no more CTAs than work
-    if (need < blocks) blocks = need > 0 ? need : 1;
-    fn<<<(unsigned)blocks, nthreads, smem, stream>>>(prm);
+    // one CTA per SM even for few workunits: warps without a workunit start by
+    // taking donated subtrees from the device-wide pool
+    void *pool = nullptr;
+    if ((e = cudaMallocAsync(&pool, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(pool)");
+    if ((e = cudaMemsetAsync(pool, 0, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(pool)");
+    Params q = prm;
+    q.pool = (uint32_t *)pool;
+    fn<<<(unsigned)sms, nthreads, smem, stream>>>(q);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "kernel launch");
+    if ((e = cudaFreeAsync(pool, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(pool)");
     return DLS_OK;
 }
 
@@ -654,10 +769,16 @@ namespace {
 constexpr int64_t kRefineTarget = 1200000;
 constexpr int kMinSearchLevels = 8;
 
-struct DevBuf {
+// Device scratch of the synchronous dls_count, cached per device (grow-only) so
+// repeated calls do not pay cudaMalloc/cudaFree; the mutex serialises callers.
+struct Workspace {
+    std::mutex mu;
     void *p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    size_t cap = 0;
 };
+Workspace g_ws[64];
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
@@ -715,27 +836,35 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
     }
     const bool refined = depth_run != depth;
 
-    DevBuf b_pre, b_cnt, b_par, b_stats;
-    const uint8_t *d_pre = src;
-    if (n_rec > 0 && (refined || !in_dev)) {
-        if ((e = cudaMalloc(&b_pre.p, (size_t)n_rec * nn)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-        if ((e = cudaMemcpyAsync(b_pre.p, src, (size_t)n_rec * nn, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-            return cuda_fail(e, "cudaMemcpyAsync(H2D)");
-        d_pre = (const uint8_t *)b_pre.p;
-    }
-    u64 *d_counts = (u64 *)out_counts;
     const bool counts_host = out_counts && n_prefix > 0 && !is_device_ptr(out_counts);
-    if (counts_host) {
-        if ((e = cudaMalloc(&b_cnt.p, (size_t)n_prefix * sizeof(u64))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-        d_counts = (u64 *)b_cnt.p;
+    const bool stage_records = n_rec > 0 && (refined || !in_dev);
+    // workspace layout: stats | counts (host output) | parent map | records
+    const size_t off_cnt = align256(DLS_STATS_WORDS * sizeof(u64));
+    const size_t off_par = off_cnt + align256(counts_host ? (size_t)n_prefix * sizeof(u64) : 0);
+    const size_t off_rec = off_par + align256(refined ? (size_t)n_rec * sizeof(uint32_t) : 0);
+    const size_t need = off_rec + (stage_records ? (size_t)n_rec * nn : 0);
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    Workspace &ws = g_ws[dev & 63];
+    std::lock_guard<std::mutex> lock(ws.mu);
+    if (ws.cap < need) {
+        if (ws.p) { cudaStreamSynchronize(s); cudaFree(ws.p); ws.p = nullptr; ws.cap = 0; }
+        const size_t cap = need + need / 4;
+        if ((e = cudaMalloc(&ws.p, cap)) != cudaSuccess) { ws.p = nullptr; return cuda_fail(e, "cudaMalloc(workspace)"); }
+        ws.cap = cap;
     }
-    if (refined) {
-        if ((e = cudaMalloc(&b_par.p, (size_t)n_rec * sizeof(uint32_t))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-        if ((e = cudaMemcpyAsync(b_par.p, h_parent.data(), (size_t)n_rec * sizeof(uint32_t), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    char *const base = (char *)ws.p;
+    const uint8_t *d_pre = src;
+    if (stage_records) {
+        if ((e = cudaMemcpyAsync(base + off_rec, src, (size_t)n_rec * nn, cudaMemcpyHostToDevice, s)) != cudaSuccess)
             return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+        d_pre = (const uint8_t *)(base + off_rec);
     }
-    if ((e = cudaMalloc(&b_stats.p, DLS_STATS_WORDS * sizeof(u64))) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    u64 *d_stats = (u64 *)b_stats.p;
+    u64 *d_counts = counts_host ? (u64 *)(base + off_cnt) : (u64 *)out_counts;
+    if (refined &&
+        (e = cudaMemcpyAsync(base + off_par, h_parent.data(), (size_t)n_rec * sizeof(uint32_t), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    u64 *d_stats = (u64 *)base;
     if ((e = cudaMemsetAsync(d_stats, 0, DLS_STATS_WORDS * sizeof(u64), s)) != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync(stats)");
     if (d_counts && n_prefix > 0 &&
@@ -745,7 +874,7 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
         prm.prefixes = d_pre;
         prm.n_prefix = n_rec;
         prm.counts = d_counts;
-        prm.parent = refined ? (const uint32_t *)b_par.p : nullptr;
+        prm.parent = refined ? (const uint32_t *)(base + off_par) : nullptr;
         prm.stats = d_stats;
         if ((rc = launch(n, symmetric, prm, s))) { cudaStreamSynchronize(s); return rc; }
     }

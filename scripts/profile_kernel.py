@@ -41,7 +41,7 @@ def main():
         st = stats.cpu().tolist()
         ms = e0.elapsed_time(e1)
         out.append({"launch": i, "ms": ms, "count": st[0], "nodes": st[1] + st[0], "err": st[2],
-                    "donations": st[4], "squares_per_s": st[0] / ms * 1e3, "nodes_per_s": (st[1] + st[0]) / ms * 1e3})
+                    "donations": st[4], "lane_util": st[5] / max(st[6], 1), "squares_per_s": st[0] / ms * 1e3, "nodes_per_s": (st[1] + st[0]) / ms * 1e3})
     print(json.dumps({"n": a.n, "vs": a.vs, "depth": d, "n_prefix": int(recs.shape[0]), "launches": out}))
 
 
