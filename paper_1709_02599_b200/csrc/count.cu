@@ -48,7 +48,7 @@ constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than thi
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Device-wide donation pool (global memory, one per launch): control words
 // [0] active warps, [1] waiting warps, [2] head (claimed), [3] tail (reserved),
-// then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1/w2 = pid,
+// then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1 = pid,
 // w3 = split level | untried siblings << 16, w4.. = the values (bit indices) of
 // levels 1..split-1, 4 bits each.
 constexpr uint32_t kPoolSlots = 16384;
@@ -214,18 +214,19 @@ __host__ __device__ inline bool pat_bit(const u64 *pat, int c) {
 // pattern cells assigned, values < N, no repeated value in a row, column or
 // diagonal, and (VS) mirror consistency LS[i][N-1-j] = N-1-LS[i][j].
 template <int N, bool VS>
-__device__ __noinline__ bool load_prefix(const uint8_t *__restrict__ rec, const u64 pat0, const u64 pat1,
-                                         Masks<N, VS> &st) {
+__device__ __forceinline__ bool load_prefix(const uint8_t *__restrict__ rec, const u64 pat0, const u64 pat1,
+                                            Masks<N, VS> &st) {
     typedef Geo<N, VS> G;
     const u64 pat[2] = {pat0, pat1};
-    uint32_t cm[N], sc[G::NC > 0 ? G::NC : 1];
+    uint32_t cm[N];                                 // value bits per column (validation)
+    uint32_t sc[VS ? (G::NC > 0 ? G::NC : 1) : 1];  // VS: position bits of the left columns
     uint32_t md = 0, ad = 0;
     bool ok = true;
     st.clear();
 #pragma unroll
     for (int j = 0; j < N; ++j) cm[j] = 0;
 #pragma unroll
-    for (int j = 0; j < G::NC; ++j) sc[j] = 0;
+    for (int j = 0; j < (VS ? G::NC : 1); ++j) sc[j] = 0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         uint32_t rm = 0, sr = 0;
@@ -250,24 +251,16 @@ __device__ __noinline__ bool load_prefix(const uint8_t *__restrict__ rec, const 
                         sr |= G::rowbit(pb);
                         sc[j < G::NC ? j : 0] |= pb;
                     }
-                } else {
-                    sr |= b;
-                    sc[j < G::NC ? j : 0] |= b;
                 }
             }
         }
-        st.set_row(i, sr);
+        st.set_row(i, VS ? sr : rm);
     }
 #pragma unroll
-    for (int j = 0; j < G::NC; ++j) st.set_col(j, sc[j]);
+    for (int j = 0; j < G::NC; ++j) st.set_col(j, VS ? sc[VS ? j : 0] : cm[j]);
     return ok;
 }
 
-__device__ __forceinline__ u64 warp_sum(u64 v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(kFull, v, o);
-    return v;
-}
 
 // Shared memory of one CTA (one CTA per SM, NT lanes):
 //   per transition u = t+1 (t = -1 .. L) a block of 32 toggle entries (uint4)
@@ -327,21 +320,32 @@ dls_search_kernel(const __grid_constant__ Params p) {
     st.clear();
     int lvl = 0;           // 0: idle / finished, 1..L: searching level lvl
     uint32_t cur = 0;      // untried candidates at level lvl
-    long long pid = -1;    // prefix being searched
+    int pid = -1;          // prefix being searched (n_prefix < 2^31)
     u64 cnt = 0;           // completions found for pid by this lane
-    u64 tot = 0, nodes = 0, donations = 0;
-    uint32_t bursts = 0, busy_bursts = 0;   // lane utilisation (stats[5] / stats[6])
+    // per-warp accumulators (shared memory, written by lane 0 / shared atomics):
+    // [0] squares, [1] nodes above the leaves, [2] donations, [3] busy lane-bursts,
+    // [4] lane-bursts -- keeps them out of the registers of the search loop
+    __shared__ u64 wacc[32][5];
+    u64 *const acc = wacc[tid >> 5];
+    if (lane < 5) acc[lane] = 0;
+    __syncwarp();
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
     for (;;) {
         // ------------------------------------------------ scheduling point
         if (pid >= 0 && lvl == 0) {
-            if (p.counts && cnt) atomicAdd(p.counts + (p.parent ? (long long)p.parent[pid] : pid), cnt);
-            tot += cnt;
+            if (p.counts && cnt) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), cnt);
+            if (cnt) atomicAdd(acc + 0, cnt);
             cnt = 0;
             pid = -1;
         }
+        // a lane that receives work sets pid, fills its stack slots 1..split-1 with
+        // the assigned values of the path above `split`, and sets `rest` (the
+        // untried values of level split); split = 0 marks a fresh workunit
+        bool adopt = false;
+        int split = 0;
+        uint32_t rest = 0;
         if (!qempty) {
             const unsigned idle = __ballot_sync(kFull, pid < 0);
             if (idle) {
@@ -352,23 +356,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 if (base + (u64)__popc(idle) >= n_prefix) qempty = true;
                 if (pid < 0) {
                     const u64 my = base + (u64)__popc(idle & lt_mask);
-                    if (my < n_prefix) {
-                        pid = (long long)my;
-                        const bool ok = load_prefix<N, VS>(p.prefixes + my * (u64)(N * N), p.pat[0], p.pat[1], st);
-                        if (!ok) {
-                            atomicOr(p.stats + 2, 1ull);
-                            lvl = 0;
-                            cur = 0;
-                        } else if (L == 0) {
-                            cnt = 1;   // the prefix is a complete square
-                            lvl = 0;
-                            cur = 0;
-                        } else {
-                            lvl = 1;   // enter level 1: candidates of cell(1) = transition 0
-                            const uint32_t c = st.cand(Cl[0]);   // transition 0 reads cell(1)
-                            if (L == 1) { cnt += __popc(c); cur = 0; } else { cur = c; }
-                        }
-                    }
+                    if (my < n_prefix) { pid = (int)my; adopt = true; }
                 }
             }
         }
@@ -416,69 +404,59 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     const volatile uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
                     while (slot[0] != ticket + 1u) __nanosleep(64);
                     __threadfence();
-                    pid = (long long)((u64)slot[1] | ((u64)slot[2] << 32));
+                    pid = (int)slot[1];
                     const uint32_t w3 = slot[3];
-                    const int split = (int)(w3 & 0xFFFFu);
-                    for (int l = 1; l < split; ++l) {
-                        const uint32_t v = (slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u;
-                        S[(l + 1) * kBlock] = 1u << v;
-                    }
-                    load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
-                    for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * kBlock], 0u);
-                    lvl = split;
-                    cur = w3 >> 16;
-                    cnt = 0;
+                    split = (int)(w3 & 0xFFFFu);
+                    rest = w3 >> 16;
+                    for (int l = 1; l < split; ++l)
+                        S[(l + 1) * kBlock] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
+                    adopt = true;
                 }
             } else {
                 // shallowest open level of each busy lane (its untried siblings)
-                int split = 0;
-                uint32_t rest = 0;
+                int dsplit = 0;
+                uint32_t drest = 0;
                 if (pid >= 0 && lvl > 0) {
                     for (int l = 1; l < lvl && l <= L - kMinDonateDepth; ++l) {
                         const uint32_t s = S[(l + 1) * kBlock];
-                        if (s & (s - 1u)) { split = l; rest = s & (s - 1u); break; }
+                        if (s & (s - 1u)) { dsplit = l; drest = s & (s - 1u); break; }
                     }
-                    if (!split && lvl <= L - kMinDonateDepth && (cur & (cur - 1u))) {
-                        split = lvl;
-                        rest = cur & (cur - 1u);   // keep the lowest for ourselves
+                    if (!dsplit && lvl <= L - kMinDonateDepth && (cur & (cur - 1u))) {
+                        dsplit = lvl;
+                        drest = cur & (cur - 1u);   // keep the lowest for ourselves
                     }
                 }
                 if (idle && p.donate) {
                     // ---- warp-vote donation to the idle lanes of this warp:
                     // k-th idle lane <- k-th donor lane
-                    const unsigned donors = __ballot_sync(kFull, split > 0);
+                    const unsigned donors = __ballot_sync(kFull, dsplit > 0);
                     const int pairs = min(__popc(donors), __popc(idle));
                     if (pairs) {
                         const int my_rank = __popc(idle & lt_mask);
                         int src = 0;
                         if (pid < 0 && my_rank < pairs) src = __fns(donors, 0, my_rank + 1);
                         const int dn_rank = __popc(donors & lt_mask);
-                        const int d_split = __shfl_sync(kFull, split, src);
-                        const uint32_t d_rest = __shfl_sync(kFull, rest, src);
-                        const long long d_pid = __shfl_sync(kFull, pid, src);
+                        const int d_split = __shfl_sync(kFull, dsplit, src);
+                        const uint32_t d_rest = __shfl_sync(kFull, drest, src);
+                        const int d_pid = __shfl_sync(kFull, pid, src);
                         const bool recv = pid < 0 && my_rank < pairs;
-                        const bool give = split > 0 && dn_rank < pairs;
+                        const bool give = dsplit > 0 && dn_rank < pairs;
                         if (recv) {
                             // copy the donor's path above the split level
-                            uint32_t *const Sd = stack + (tid - lane + src);
+                            const uint32_t *const Sd = stack + (tid - lane + src);
                             for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
                         }
                         __syncwarp();
                         if (give) {
-                            if (split < lvl) S[(split + 1) * kBlock] &= 0u - S[(split + 1) * kBlock];
+                            if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
                             else cur &= 0u - cur;
-                            ++donations;
                         }
+                        if (lane == 0) acc[2] += (u64)pairs;
                         if (recv) {
                             pid = d_pid;
-                            load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
-                            for (int l = 1; l < d_split; ++l) {
-                                const uint32_t s = S[(l + 1) * kBlock];
-                                st.toggle(Fl[l * kBlk], s & (0u - s), 0u);
-                            }
-                            lvl = d_split;
-                            cur = d_rest;
-                            cnt = 0;
+                            split = d_split;
+                            rest = d_rest;
+                            adopt = true;
                         }
                     }
                 } else if (p.donate) {
@@ -491,36 +469,61 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     feed = __shfl_sync(kFull, feed, 0);
                     if (feed) {
                         // the lane with the shallowest open level donates it
-                        const uint32_t key = split > 0 ? ((uint32_t)split << 5) | (uint32_t)lane : 0xFFFFFFFFu;
+                        const uint32_t key = dsplit > 0 ? ((uint32_t)dsplit << 5) | (uint32_t)lane : 0xFFFFFFFFu;
                         const uint32_t best = __reduce_min_sync(kFull, key);
                         if (best != 0xFFFFFFFFu && (best & 31u) == (uint32_t)lane) {
                             const uint32_t ticket = atomicAdd(pool + 3, 1u);
                             uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
-                            slot[1] = (uint32_t)((u64)pid & 0xFFFFFFFFull);
-                            slot[2] = (uint32_t)((u64)pid >> 32);
-                            slot[3] = (uint32_t)split | (rest << 16);
-                            for (int w = 0; w < (split + 6) / 8; ++w) {
+                            slot[1] = (uint32_t)pid;
+                            slot[3] = (uint32_t)dsplit | (drest << 16);
+                            for (int w = 0; w < (dsplit + 6) / 8; ++w) {
                                 uint32_t word = 0;
                                 for (int k = 0; k < 8; ++k) {
                                     const int l = 1 + w * 8 + k;
-                                    if (l < split) word |= (uint32_t)(__ffs(S[(l + 1) * kBlock]) - 1) << (4 * k);
+                                    if (l < dsplit) word |= (uint32_t)(__ffs(S[(l + 1) * kBlock]) - 1) << (4 * k);
                                 }
                                 slot[4 + w] = word;
                             }
                             __threadfence();
                             *(volatile uint32_t *)slot = ticket + 1u;
-                            if (split < lvl) S[(split + 1) * kBlock] &= 0u - S[(split + 1) * kBlock];
+                            if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
                             else cur &= 0u - cur;
-                            ++donations;
+                            atomicAdd(acc + 2, 1ull);
                         }
                     }
                 }
             }
         }
+        if (adopt) {
+            // rebuild Rows/Columns from the record, then replay the path
+            const bool ok = load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
+            cnt = 0;
+            if (split == 0) {                  // a fresh workunit from the queue
+                if (!ok) {
+                    atomicOr(p.stats + 2, 1ull);
+                    lvl = 0;
+                    cur = 0;
+                } else if (L == 0) {
+                    cnt = 1;                   // the record is a complete square
+                    lvl = 0;
+                    cur = 0;
+                } else {
+                    lvl = 1;                   // enter level 1: transition 0 reads cell(1)
+                    const uint32_t c = st.cand(Cl[0]);
+                    if (L == 1) { cnt = __popc(c); cur = 0; } else { cur = c; }
+                }
+            } else {                           // a donated subtree
+                for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * kBlock], 0u);
+                lvl = split;
+                cur = rest;
+            }
+        }
 
         // ------------------------------------------------ kBurst DFS steps
-        ++bursts;
-        busy_bursts += pid >= 0 ? 1u : 0u;
+        {
+            const unsigned busy = __ballot_sync(kFull, pid >= 0);
+            if (lane == 0) { acc[3] += (u64)__popc(busy); acc[4] += 32; }
+        }
         uint32_t cnt32 = 0, ent32 = 0;
 #pragma unroll 8
         for (int s = 0; s < kBurst; ++s) {
@@ -556,23 +559,16 @@ dls_search_kernel(const __grid_constant__ Params p) {
             lvl = nl;
         }
         cnt += cnt32;
-        nodes += ent32;
+        const uint32_t wn = __reduce_add_sync(kFull, ent32);
+        if (lane == 0) acc[1] += (u64)wn;
     }
 
     // ------------------------------------------------ block reduction, 1 atomic per block
-    __shared__ u64 red[5][32];
-    u64 v[5] = {tot, nodes, donations, busy_bursts, bursts};
-#pragma unroll
-    for (int k = 0; k < 5; ++k) v[k] = warp_sum(v[k]);
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 5; ++k) red[k][tid >> 5] = v[k];
-    }
     __syncthreads();
     if (tid == 0) {
         u64 a[5] = {0, 0, 0, 0, 0};
         for (int w = 0; w < NT / 32; ++w)
-            for (int k = 0; k < 5; ++k) a[k] += red[k][w];
+            for (int k = 0; k < 5; ++k) a[k] += wacc[w][k];
         atomicAdd(p.stats + 0, a[0]);   // squares
         atomicAdd(p.stats + 1, a[1]);   // nodes above the leaves
         atomicAdd(p.stats + 4, a[2]);   // donations
@@ -690,7 +686,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
         return cuda_fail(e, "cudaDeviceGetAttribute");
     if ((e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
         return cuda_fail(e, "cudaDeviceGetAttribute");
-    smem_max -= 1024;   // static shared memory of the kernel
+    smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators)
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     int nthreads = n <= 8 ? 1024 : 512;   // = the kernel's __launch_bounds__ (byte layout: fixed)
     while (n > 8 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
@@ -741,7 +737,7 @@ extern "C" int dls_count_async(int n, int symmetric, int fixed_first_row, int de
                                uint64_t *d_stats, void *stream) {
     int rc = have_device();
     if (rc) return rc;
-    if (n_prefix < 0 || (n_prefix > 0 && !d_prefixes) || !d_stats) {
+    if (n_prefix < 0 || n_prefix >= (int64_t)1 << 31 || (n_prefix > 0 && !d_prefixes) || !d_stats) {
         dls::set_error("dls_count_async: bad pointers / sizes");
         return DLS_E_ARG;
     }
@@ -787,7 +783,7 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
                          uint64_t *out_total, uint64_t *out_nodes, void *stream) {
     int rc = have_device();
     if (rc) return rc;
-    if (n_prefix < 0 || (n_prefix > 0 && !prefix_buf)) {
+    if (n_prefix < 0 || n_prefix >= (int64_t)1 << 31 || (n_prefix > 0 && !prefix_buf)) {
         dls::set_error("dls_count: bad pointers / sizes");
         return DLS_E_ARG;
     }
