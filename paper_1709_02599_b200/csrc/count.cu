@@ -48,6 +48,7 @@ constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than thi
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Device-wide donation pool (global memory, one per launch): control words
 // [0] active warps, [1] waiting warps, [2] head (claimed), [3] tail (reserved),
+// [4] warps registered (exit is allowed only once all warps of the grid are),
 // then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1 = pid,
 // w3 = split level | untried siblings << 16, w4.. = the values (bit indices) of
 // levels 1..split-1, 4 bits each.
@@ -87,10 +88,17 @@ struct Geo {
     static constexpr int NC = VS ? H : N;                      // tracked columns
     static constexpr uint32_t ALLN = (1u << N) - 1u;
     static constexpr uint32_t HMASK = (1u << H) - 1u;
-    static constexpr bool BYTES = N <= 8;                      // byte-field layout
-    static constexpr int RF = VS ? (H > 0 ? H : 1) : N;        // shift layout: row field width
-    static constexpr int CF = N;                               //               col field width
-    static constexpr int RPW = 64 / RF;
+    static constexpr int RF = VS ? (H > 0 ? H : 1) : N;        // row field width (bits)
+    static constexpr int CF = N;                               // column field width
+    // word-field layout: fields never straddle a 32-bit word, 2 words per unit
+    static constexpr int RPW32 = 32 / RF;
+    static constexpr int CPW32 = 32 / CF;
+    static constexpr bool FITS2 = (N + RPW32 - 1) / RPW32 <= 2 && (NC + CPW32 - 1) / CPW32 <= 2;
+    // 0: byte fields + PRMT (N <= 8); 1: word fields + funnel shift (e.g. VS N=10);
+    // 2: 64-bit words + funnel shifts (DLS N = 9, 10)
+    static constexpr int LAYOUT = N <= 8 ? 0 : (FITS2 ? 1 : 2);
+    static constexpr bool BYTES = LAYOUT == 0;
+    static constexpr int RPW = 64 / RF;                        // layout 2
     static constexpr int CPW = 64 / CF;
     static constexpr int WR = (N + RPW - 1) / RPW;
     static constexpr int WC = (NC + CPW - 1) / CPW;
@@ -108,7 +116,7 @@ struct Geo {
     }
 };
 
-template <int N, bool VS, bool BYTES = Geo<N, VS>::BYTES>
+template <int N, bool VS, int LAYOUT = Geo<N, VS>::LAYOUT>
 struct Masks;
 
 // N <= 8: row r is byte r&3 of R[r>>2], column c is byte c&3 of C[c>>2].
@@ -124,7 +132,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 }
 
 template <int N, bool VS>
-struct Masks<N, VS, true> {
+struct Masks<N, VS, 0> {
     typedef Geo<N, VS> G;
     typedef uint2 CT;
     uint32_t R0, R1, C0, C1;
@@ -155,11 +163,52 @@ struct Masks<N, VS, true> {
     }
 };
 
+// Word fields (e.g. vertical symmetry, N = 10): row r is field r % RPW32 of
+// R[r / RPW32] (RF bits each), column c field c % CPW32 of C[c / CPW32]; no field
+// straddles a word, so toggles are IMADs as in the byte layout, and a field is read
+// with one 64-bit funnel shift of the word pair.
+// Tab: w0..w3 = multipliers (1 << field offset, in the word holding the field);
+//      w4, w5 = bit offsets (0..63) of cell(t+1)'s row/col field in the pair;
+//      w6 = leaf, w7 = not leaf.
+template <int N, bool VS>
+struct Masks<N, VS, 1> {
+    typedef Geo<N, VS> G;
+    typedef uint4 CT;
+    uint32_t R0, R1, C0, C1;
+
+    __device__ __forceinline__ void clear() { R0 = R1 = C0 = C1 = 0; }
+    __device__ __forceinline__ void set_row(int r, uint32_t m) {
+        const int o = (r % G::RPW32) * G::RF;
+        if (r / G::RPW32 == 0) R0 |= m << o; else R1 |= m << o;
+    }
+    __device__ __forceinline__ void set_col(int c, uint32_t m) {
+        const int o = (c % G::CPW32) * G::CF;
+        if (c / G::CPW32 == 0) C0 |= m << o; else C1 |= m << o;
+    }
+    __device__ __forceinline__ void toggle(const uint4 &f, uint32_t bnew, uint32_t bold) {
+        const uint32_t dc = bnew - bold;
+        const uint32_t dr = VS ? G::rowbit(bnew) - G::rowbit(bold) : dc;
+        R0 += dr * f.x;
+        R1 += dr * f.y;
+        C0 += dc * f.z;
+        C1 += dc * f.w;
+    }
+    __device__ __forceinline__ uint32_t cand(const uint4 &c) const {
+        const uint32_t r = G::expand_row((uint32_t)((((u64)R1 << 32) | R0) >> c.x));
+        const uint32_t k = (uint32_t)((((u64)C1 << 32) | C0) >> c.y);
+        return G::ALLN & ~(r | k);
+    }
+    __device__ __forceinline__ static void leaf_flags(const uint4 &c, int, int, uint32_t &leaf, uint32_t &notleaf) {
+        leaf = c.z;
+        notleaf = c.w;
+    }
+};
+
 // N = 9, 10: row/column fields packed in 64-bit words (W of them), moved by
 // funnel shifts.  Tab: w0..w3 = row shift, row word, col shift, col word of
 // cell(t); w4..w7 = the same of cell(t+1).
 template <int N, bool VS>
-struct Masks<N, VS, false> {
+struct Masks<N, VS, 2> {
     typedef Geo<N, VS> G;
     u64 R[G::WR];
     u64 C[G::WC];
@@ -205,6 +254,12 @@ struct Masks<N, VS, false> {
     }
     typedef uint4 CT;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __host__ __device__ inline bool pat_bit(const u64 *pat, int c) {
     return (pat[c >> 6] >> (c & 63)) & 1ull;
@@ -270,13 +325,13 @@ __device__ __forceinline__ bool load_prefix(const uint8_t *__restrict__ rec, con
 template <int N, bool VS>
 struct Layout {
     static constexpr bool BYTES = Geo<N, VS>::BYTES;
-    static constexpr int NT_FIXED = BYTES ? 1024 : 0;        // lanes per CTA (0 = runtime)
+    static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT != 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
     static constexpr int CTW = BYTES ? 2 : 4;                 // words of a read entry
     static constexpr int BLK_WORDS = 32 * (4 + CTW);          // words per transition block
 };
 
 template <int N, bool VS>
-__global__ void __launch_bounds__(Geo<N, VS>::BYTES ? 1024 : 512, 1)
+__global__ void __launch_bounds__(Geo<N, VS>::LAYOUT != 2 ? 1024 : 512, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
@@ -313,7 +368,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const char *const Cb = reinterpret_cast<const char *>(Cl);
 
     uint32_t *const pool = p.pool;
-    if (lane == 0) atomicAdd(pool + 0, 1u);        // this warp is active
+    const uint32_t total_warps = gridDim.x * (uint32_t)(NT / 32);
+    if (lane == 0) {
+        atomicAdd(pool + 0, 1u);                   // this warp is active
+        __threadfence();
+        atomicAdd(pool + 4, 1u);                   // ... and registered
+    }
     bool waiting = false;
 
     M st;
@@ -321,13 +381,14 @@ dls_search_kernel(const __grid_constant__ Params p) {
     int lvl = 0;           // 0: idle / finished, 1..L: searching level lvl
     uint32_t cur = 0;      // untried candidates at level lvl
     int pid = -1;          // prefix being searched (n_prefix < 2^31)
-    u64 cnt = 0;           // completions found for pid by this lane
+    uint32_t cnt = 0;      // completions found for pid by this lane since the last flush
     // per-warp accumulators (shared memory, written by lane 0 / shared atomics):
     // [0] squares, [1] nodes above the leaves, [2] donations, [3] busy lane-bursts,
     // [4] lane-bursts -- keeps them out of the registers of the search loop
-    __shared__ u64 wacc[32][5];
+    // [5] (lane 0 only): ns between pool polls of this warp while idle
+    __shared__ u64 wacc[32][6];
     u64 *const acc = wacc[tid >> 5];
-    if (lane < 5) acc[lane] = 0;
+    if (lane < 6) acc[lane] = 0;
     __syncwarp();
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
@@ -335,8 +396,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
     for (;;) {
         // ------------------------------------------------ scheduling point
         if (pid >= 0 && lvl == 0) {
-            if (p.counts && cnt) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), cnt);
-            if (cnt) atomicAdd(acc + 0, cnt);
+            if (p.counts && cnt) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
+            if (cnt) atomicAdd(acc + 0, (u64)cnt);
             cnt = 0;
             pid = -1;
         }
@@ -371,11 +432,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         atomicAdd(pool + 1, 1u);
                         __threadfence();
                         atomicSub(pool + 0, 1u);
+                        acc[5] = 128;
                     }
-                    if (atomicAdd(pool + 3, 0u) != atomicAdd(pool + 2, 0u)) {
+                    // poll with loads; atomics only when something is pending
+                    if (ld_acquire(pool + 3) != ld_acquire(pool + 2)) {
                         atomicAdd(pool + 0, 1u);           // tentatively active before claiming
                         for (int tries = 0; tries < 8 && !got; ++tries) {
-                            const uint32_t h = atomicAdd(pool + 2, 0u), t = atomicAdd(pool + 3, 0u);
+                            const uint32_t h = ld_acquire(pool + 2), t = ld_acquire(pool + 3);
                             const int avail = (int)(t - h);
                             if (avail <= 0) break;
                             const uint32_t k = min(avail, 32);
@@ -385,9 +448,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         else atomicSub(pool + 0, 1u);
                     }
                     if (!got) {
-                        const uint32_t a = atomicAdd(pool + 0, 0u);
+                        // every warp registered, none active, nothing pending: the
+                        // search is complete (only active warps publish subtrees)
+                        const uint32_t reg = ld_acquire(pool + 4);
                         __threadfence();
-                        done = (a == 0u && atomicAdd(pool + 2, 0u) == atomicAdd(pool + 3, 0u)) ? 1u : 0u;
+                        const uint32_t a = ld_acquire(pool + 0);
+                        __threadfence();
+                        done = (reg == total_warps && a == 0u && ld_acquire(pool + 2) == ld_acquire(pool + 3)) ? 1u : 0u;
                     }
                 }
                 got = __shfl_sync(kFull, got, 0);
@@ -396,7 +463,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 if (done) break;
                 waiting = got == 0;
                 if (!got) {
-                    __nanosleep(1000);
+                    if (lane == 0) {
+                        const uint32_t ns = (uint32_t)acc[5];
+                        __nanosleep(ns);
+                        acc[5] = min(ns * 2u, 8192u);
+                    }
+                    __syncwarp();
                     continue;
                 }
                 if ((uint32_t)lane < got) {
@@ -426,52 +498,51 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         drest = cur & (cur - 1u);   // keep the lowest for ourselves
                     }
                 }
-                if (idle && p.donate) {
+                unsigned donors = __ballot_sync(kFull, dsplit > 0);
+                if (idle && donors && p.donate) {
                     // ---- warp-vote donation to the idle lanes of this warp:
                     // k-th idle lane <- k-th donor lane
-                    const unsigned donors = __ballot_sync(kFull, dsplit > 0);
                     const int pairs = min(__popc(donors), __popc(idle));
-                    if (pairs) {
-                        const int my_rank = __popc(idle & lt_mask);
-                        int src = 0;
-                        if (pid < 0 && my_rank < pairs) src = __fns(donors, 0, my_rank + 1);
-                        const int dn_rank = __popc(donors & lt_mask);
-                        const int d_split = __shfl_sync(kFull, dsplit, src);
-                        const uint32_t d_rest = __shfl_sync(kFull, drest, src);
-                        const int d_pid = __shfl_sync(kFull, pid, src);
-                        const bool recv = pid < 0 && my_rank < pairs;
-                        const bool give = dsplit > 0 && dn_rank < pairs;
-                        if (recv) {
-                            // copy the donor's path above the split level
-                            const uint32_t *const Sd = stack + (tid - lane + src);
-                            for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
-                        }
-                        __syncwarp();
-                        if (give) {
-                            if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
-                            else cur &= 0u - cur;
-                        }
-                        if (lane == 0) acc[2] += (u64)pairs;
-                        if (recv) {
-                            pid = d_pid;
-                            split = d_split;
-                            rest = d_rest;
-                            adopt = true;
-                        }
+                    const int my_rank = __popc(idle & lt_mask);
+                    int src = 0;
+                    if (pid < 0 && my_rank < pairs) src = __fns(donors, 0, my_rank + 1);
+                    const int dn_rank = __popc(donors & lt_mask);
+                    const int d_split = __shfl_sync(kFull, dsplit, src);
+                    const uint32_t d_rest = __shfl_sync(kFull, drest, src);
+                    const int d_pid = __shfl_sync(kFull, pid, src);
+                    const bool recv = pid < 0 && my_rank < pairs;
+                    const bool give = dsplit > 0 && dn_rank < pairs;
+                    if (recv) {
+                        // copy the donor's path above the split level
+                        const uint32_t *const Sd = stack + (tid - lane + src);
+                        for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
                     }
-                } else if (p.donate) {
-                    // ---- no idle lane here: feed the device-wide pool if a warp waits
+                    __syncwarp();
+                    if (give) {
+                        if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
+                        else cur &= 0u - cur;
+                        dsplit = 0;
+                    }
+                    if (lane == 0) acc[2] += (u64)pairs;
+                    if (recv) {
+                        pid = d_pid;
+                        split = d_split;
+                        rest = d_rest;
+                        adopt = true;
+                    }
+                    donors = __ballot_sync(kFull, dsplit > 0);
+                }
+                if (donors && p.donate) {
+                    // ---- donors left over: feed the device-wide pool if a warp waits
                     uint32_t feed = 0;
-                    if (lane == 0) {
-                        const volatile uint32_t *vp = pool;
-                        feed = (vp[1] != 0u && (int)(vp[3] - vp[2]) < (int)kPoolLimit) ? 1u : 0u;
-                    }
+                    if (lane == 0)
+                        feed = (ld_acquire(pool + 1) != 0u && (int)(ld_acquire(pool + 3) - ld_acquire(pool + 2)) < (int)kPoolLimit) ? 1u : 0u;
                     feed = __shfl_sync(kFull, feed, 0);
                     if (feed) {
                         // the lane with the shallowest open level donates it
                         const uint32_t key = dsplit > 0 ? ((uint32_t)dsplit << 5) | (uint32_t)lane : 0xFFFFFFFFu;
                         const uint32_t best = __reduce_min_sync(kFull, key);
-                        if (best != 0xFFFFFFFFu && (best & 31u) == (uint32_t)lane) {
+                        if ((best & 31u) == (uint32_t)lane) {
                             const uint32_t ticket = atomicAdd(pool + 3, 1u);
                             uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
                             slot[1] = (uint32_t)pid;
@@ -541,7 +612,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
             const uint4 f = *reinterpret_cast<const uint4 *>(Fb + toff);
             const CT cs = *reinterpret_cast<const CT *>(Cb + toff);
-            if constexpr (VS || !Geo<N, VS>::BYTES) {
+            if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
                 st.toggle(f, dn ? b : sb, dn ? 0u : bb);                          // mark / unmark
             } else {
                 const uint32_t d = dn ? b : sb - bb;                              // mark / unmark
@@ -559,6 +630,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
             lvl = nl;
         }
         cnt += cnt32;
+        if (cnt >= 0x80000000u) {          // flush before 32 bits could overflow
+            if (p.counts) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
+            atomicAdd(acc + 0, (u64)cnt);
+            cnt = 0;
+        }
         const uint32_t wn = __reduce_add_sync(kFull, ent32);
         if (lane == 0) acc[1] += (u64)wn;
     }
@@ -604,12 +680,22 @@ int cuda_fail(cudaError_t e, const char *what) {
 }
 
 // Host mirror of the device layouts: the per-transition table entries.
+int layout_of(int n, bool vs) {
+    const int h = n / 2;
+    const int rf = vs ? (h > 0 ? h : 1) : n, cf = n, nc = vs ? h : n;
+    const int rpw32 = 32 / rf, cpw32 = 32 / cf;
+    const bool fits2 = (n + rpw32 - 1) / rpw32 <= 2 && (nc + cpw32 - 1) / cpw32 <= 2;
+    return n <= 8 ? 0 : (fits2 ? 1 : 2);
+}
+
 void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
     const int L = (int)level_cells.size();
-    const bool bytes = n <= 8;
+    const int lay = layout_of(n, vs);
+    const bool bytes = lay == 0;
     const int h = n / 2;
     const int rf = vs ? (h > 0 ? h : 1) : n, cf = n;
     const int rpw = 64 / rf, cpw = 64 / cf;
+    const int rpw32 = 32 / rf, cpw32 = 32 / cf;
     auto cell_of = [&](int l) { return level_cells[l - 1]; };   // level l = 1..L
     for (int t = -1; t <= L; ++t) {
         Tab &e = tab[t + 1];
@@ -619,6 +705,9 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             if (bytes) {
                 (i < 4 ? e.w[0] : e.w[1]) = 1u << (8 * (i & 3));
                 (j < 4 ? e.w[2] : e.w[3]) = 1u << (8 * (j & 3));
+            } else if (lay == 1) {
+                (i / rpw32 == 0 ? e.w[0] : e.w[1]) = 1u << ((i % rpw32) * rf);
+                (j / cpw32 == 0 ? e.w[2] : e.w[3]) = 1u << ((j % cpw32) * cf);
             } else {
                 e.w[0] = (uint32_t)((i % rpw) * rf);
                 e.w[1] = (uint32_t)(i / rpw);
@@ -632,6 +721,12 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
                 const bool leaf = t + 1 == L;
                 e.w[4] = (uint32_t)i | (leaf ? 1u << 16 : 0u);
                 e.w[5] = (uint32_t)j | (leaf ? 0u : 1u << 16);
+            } else if (lay == 1) {
+                const bool leaf = t + 1 == L;
+                e.w[4] = (uint32_t)(32 * (i / rpw32) + (i % rpw32) * rf);
+                e.w[5] = (uint32_t)(32 * (j / cpw32) + (j % cpw32) * cf);
+                e.w[6] = leaf ? 1u : 0u;
+                e.w[7] = leaf ? 0u : 1u;
             } else {
                 e.w[4] = (uint32_t)((i % rpw) * rf);
                 e.w[5] = (uint32_t)(i / rpw);
@@ -672,7 +767,7 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
 }
 
 size_t smem_bytes(int n, bool vs, int L, int nthreads) {
-    const size_t ct = n <= 8 ? 8 : 16;
+    const size_t ct = layout_of(n, vs) == 0 ? 8 : 16;
     return (size_t)(L + 2) * 32 * (16 + ct) + (size_t)(L + 2) * nthreads * sizeof(uint32_t);
 }
 
@@ -688,8 +783,9 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
         return cuda_fail(e, "cudaDeviceGetAttribute");
     smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators)
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
-    int nthreads = n <= 8 ? 1024 : 512;   // = the kernel's __launch_bounds__ (byte layout: fixed)
-    while (n > 8 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
+    const int lay = layout_of(n, vs);
+    int nthreads = lay != 2 ? 1024 : 512;   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
+    while (lay == 2 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
     const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)

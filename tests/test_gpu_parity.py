@@ -254,3 +254,32 @@ def test_repeatable():
     a = _gpu(n, False, recs, d)
     b = _gpu(n, False, recs, d)
     assert (a[0] == b[0]).all() and a[1:] == b[1:]
+
+
+@pytest.mark.parametrize("n,vs,k", [(7, False, 3), (8, False, 2), (8, True, 5), (10, True, 1)])
+def test_few_workunits_spread_by_device_pool(n, vs, k):
+    """dls_count_async does no host refinement: k workunits start on k lanes and
+    reach the rest of the GPU only through warp donation and the device-wide pool."""
+    import torch
+    d = D.default_split_depth(n, vs)
+    if n == 10:
+        recs = synth.diagonal_prefixes(synth.SEED_VS10, n, 3, vs=True)
+        recs = recs[:k]
+        # deepen by one row so the oracle finishes in seconds
+        order = oracle.plan(n, vs)
+        kids = oracle.prefixes(n, vs, synth.to_int_grid(recs[0]), order[d:], 6)
+        recs = np.where(kids[:k] < 0, 255, kids[:k]).astype(np.uint8)
+        d += 6
+    else:
+        recs = D.dls_split(n, d, vs)
+        rng = np.random.default_rng(n)
+        recs = recs[rng.choice(len(recs), k, replace=False)]
+    dev = torch.from_numpy(np.ascontiguousarray(recs)).cuda()
+    out = torch.zeros(k, dtype=torch.int64, device="cuda")
+    stats = torch.zeros(B.DLS_STATS_WORDS, dtype=torch.int64, device="cuda")
+    D.dls_count_async(n, d, dev, out, stats, vs, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want, want_nodes = _oracle_per_prefix(n, vs, recs, d)
+    assert (out.cpu().numpy().astype(np.uint64) == want).all()
+    st = stats.cpu().tolist()
+    assert st[2] == 0 and st[0] == int(want.sum()) and st[1] + st[0] == want_nodes
