@@ -88,6 +88,19 @@ int64_t dls_split(int n, int symmetric, int fixed_first_row, int depth,
                   uint8_t *out_prefixes, int64_t capacity);
 
 /*
+ * dls_refine -- the same decomposition applied below given records: every
+ * consistent assignment of plan cells [depth, depth2) below each of the n_in
+ * depth-`depth` records `in` (host), in record order then depth-first order.
+ *   out            host, capacity*n*n bytes or NULL; parent: host, capacity
+ *                  uint32 (index of the record each output extends) or NULL.
+ * Returns the total number of output records (may exceed capacity), DLS_E_ARG, or
+ * DLS_E_PREFIX if some input record is not a consistent depth-`depth` prefix.
+ */
+int64_t dls_refine(int n, int symmetric, int fixed_first_row, int depth,
+                   const uint8_t *in, int64_t n_in, int depth2,
+                   uint8_t *out, uint32_t *parent, int64_t capacity);
+
+/*
  * dls_count -- exhaustive completion count of every prefix (Alg. 4, P:235-258,
  * run on the B200: one prefix per lane of a persistent sm_100a kernel, an
  * explicit per-lane stack, a global atomic work queue and warp-level subtree
@@ -117,7 +130,8 @@ int dls_count(int n, int symmetric, int fixed_first_row, int depth,
  *                  [1] + [0] when depth < n_steps), [2] prefix-error flag
  *                  (nonzero = some record was inconsistent), [3] work-queue
  *                  cursor, [4] subtree donations, [5] busy lane-bursts,
- *                  [6] lane-bursts (lane utilisation = [5]/[6]), [7] reserved.
+ *                  [6] lane-bursts (lane utilisation = [5]/[6]), [7] subtrees
+ *                  published to the device-wide donation pool.
  * Returns DLS_OK or DLS_E_ARG/DLS_E_CUDA/DLS_E_NODEVICE for launch-time errors.
  */
 #define DLS_STATS_WORDS 8

@@ -60,6 +60,12 @@ def _load():
         lib.oracle_squares.restype = ctypes.c_longlong
         lib.oracle_plan.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip]
         lib.oracle_plan.restype = ctypes.c_int
+        lib.oracle_canonize.argtypes = [ctypes.c_int, ctypes.c_int, ip]
+        lib.oracle_canonize.restype = ctypes.c_longlong
+        llp = ctypes.POINTER(ctypes.c_longlong)
+        lib.oracle_classes.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ip, llp,
+                                       ctypes.c_longlong, llp]
+        lib.oracle_classes.restype = ctypes.c_longlong
         _lib = lib
     return _lib
 
@@ -252,3 +258,51 @@ def vs_first_row_multiplier(n: int) -> int:
     if n % 2:
         return 0
     return math.factorial(n // 2) * 2 ** (n // 2)
+
+
+# ---------------------------------------------------------------- symmetry breaking (Section 4)
+
+def hourglass_cells(n: int) -> List[int]:
+    """Cells of a hourglass design other than row 0: both diagonals, then
+    row N-1, each in row-major order."""
+    diag = [i * n + j for i in range(1, n) for j in range(n) if i == j or i + j == n - 1]
+    last = [(n - 1) * n + j for j in range(n) if (n - 1) * n + j not in diag]
+    return diag + last
+
+
+def hourglasses(n: int, vs: bool = False) -> np.ndarray:
+    """All hourglass designs with row 0 = 0..N-1 (oracle prefix enumeration)."""
+    cells = hourglass_cells(n)
+    if vs:
+        cells = [c for c in cells if 2 * (c % n) <= n - 1]
+    return prefixes(n, vs, first_row_grid(n), cells, len(cells))
+
+
+def canonize(n: int, vs: bool, grid: np.ndarray) -> int:
+    """Alg. 5: 0 if ``grid`` is not the canonic form of its class,
+    else the number of distinct designs in its class."""
+    g, gp = _iarr(np.asarray(grid).reshape(-1))
+    return int(_load().oracle_canonize(n, int(bool(vs)), gp))
+
+
+def hourglass_classes(n: int, vs: bool = False, keep: bool = True):
+    """Canonic hourglass designs and their class sizes (Alg. 5/6).
+    Returns (reps (k, n, n) int32 or None, mult (k,) int64 or None, n_hourglasses)."""
+    lib = _load()
+    cells = hourglass_cells(n)
+    if vs:
+        cells = [c for c in cells if 2 * (c % n) <= n - 1]
+    g, gp = _iarr(first_row_grid(n).reshape(-1))
+    o, op = _iarr(cells)
+    nd = ctypes.c_longlong(0)
+    llp = ctypes.POINTER(ctypes.c_longlong)
+    k = lib.oracle_classes(n, int(bool(vs)), gp, op, len(cells), None, None, 0, ctypes.byref(nd))
+    if k < 0:
+        raise ValueError("oracle_classes failed: %d" % k)
+    if not keep:
+        return None, None, int(nd.value)
+    reps = np.zeros((max(k, 1), n * n), dtype=np.int32)
+    mult = np.zeros(max(k, 1), dtype=np.int64)
+    lib.oracle_classes(n, int(bool(vs)), gp, op, len(cells), reps.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                       mult.ctypes.data_as(llp), k, ctypes.byref(nd))
+    return reps[:k].reshape(-1, n, n), mult[:k], int(nd.value)

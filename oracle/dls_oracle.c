@@ -23,6 +23,9 @@
  *   oracle_prefixes  -- all consistent assignments of the first `depth` cells of an
  *                       order (workunit decomposition)
  *   oracle_squares   -- writes out every completion (for square-by-square checks)
+ *   oracle_canonize  -- M-transformations + canonic form of a hourglass design
+ *                       (Section 4, Alg. 5)
+ *   oracle_classes   -- canonic hourglass designs with class sizes (Alg. 6 outer loops)
  *
  * Vertical symmetry: with vs != 0 only left-half cells (j < N/2 ... or
  * j <= N-1-j) appear in an order; placing v at (i,j) also places N-1-v at
@@ -51,7 +54,12 @@ typedef struct {
     long long emit_cap;
     long long emitted;
     int emit_depth;               /* stop depth for prefix enumeration (-1 = full) */
+    int canon;                    /* 1: at the stop depth canonise (Alg. 5) instead of emitting */
+    long long classes;            /* canonical designs found */
+    long long *mult_out;          /* their class sizes (up to emit_cap) */
 } oracle_state;
+
+long long oracle_canonize(int n, int vs, const int *g);
 
 /* Does placing value v at (i,j) clash with an already assigned cell of the same
  * row, column, main diagonal (i==j) or main antidiagonal (i+j==n-1)?  (Alg. 2,
@@ -118,6 +126,21 @@ static void fill(oracle_state *s, int step)
     int stop = s->emit_depth >= 0 ? s->emit_depth : s->n_order;
     if (step == stop) {
         s->count++;                      /* SquaresCnt++  */
+        if (s->canon) {
+            int g[MAXN * MAXN], i, j;
+            long long m;
+            for (i = 0; i < s->n; i++)
+                for (j = 0; j < s->n; j++) g[i * s->n + j] = s->ls[i][j];
+            m = oracle_canonize(s->n, s->vs, g);
+            if (m > 0) {
+                if (s->emit && s->classes < s->emit_cap) {
+                    memcpy(s->emit + s->classes * (long long)s->n * s->n, g, sizeof(int) * s->n * s->n);
+                    s->mult_out[s->classes] = m;
+                }
+                s->classes++;
+            }
+            return;
+        }
         if (s->emit) emit_grid(s);
         else if (s->emit_depth >= 0) s->emitted++;
         return;
@@ -269,4 +292,117 @@ int oracle_plan(int n, int vs, const int *pre, int *order)
         order[steps++] = pick;
     }
     return steps;
+}
+
+/* ------------------------------------------------------------------------ */
+/* M-transformations and canonisation of hourglass designs (Section 4,       */
+/* P:297-438, Alg. 5).                                                       */
+/*                                                                            */
+/* An index map sigma acts on rows and columns alike: the pairs {k, N-1-k}   */
+/* (k < h = floor(N/2)) are permuted by a permutation pi of 0..h-1 with      */
+/* pi(0) = 0 (third type: row 0 may only meet row N-1), then the pairs */
+/* in the subset `swap` have their two members exchanged (second type);*/
+/* for odd N the middle index stays.  Optionally columns are then mirrored    */
+/* (first type, vertical mirror; with symmetric pair swaps it also     */
+/* yields the horizontal mirror).  The image is renamed so that row 0 reads  */
+/* 0..N-1, empty cells stay empty.                            */
+/* ------------------------------------------------------------------------ */
+
+static void apply_m(int n, const int *g, const int *pi, int swap, int mirror, int *out)
+{
+    int sigma[MAXN], i, j, h = n / 2;
+    int ren[MAXN];
+    for (i = 0; i < n; i++) sigma[i] = i;
+    for (i = 0; i < h; i++) {            /* pair i -> pair pi[i], then optional swap */
+        int a = pi[i], lo = a, hi = n - 1 - a;
+        if (swap & (1 << a)) { int t = lo; lo = hi; hi = t; }
+        sigma[i] = lo;
+        sigma[n - 1 - i] = hi;
+    }
+    for (i = 0; i < n * n; i++) out[i] = -1;
+    for (i = 0; i < n; i++)
+        for (j = 0; j < n; j++) {
+            int v = g[i * n + j];
+            int ti = sigma[i], tj = sigma[j];
+            if (mirror) tj = n - 1 - tj;
+            out[ti * n + tj] = v;
+        }
+    /* rename symbols so that row 0 is 0..N-1 (row 0 of an image is a full row) */
+    for (j = 0; j < n; j++) ren[j] = -1;
+    for (j = 0; j < n; j++) if (out[j] >= 0) ren[out[j]] = j;
+    for (i = 0; i < n * n; i++) if (out[i] >= 0) out[i] = ren[out[i]];
+}
+
+static int lex_cmp(int n, const int *a, const int *b)
+{
+    int k;
+    for (k = 0; k < n * n; k++) {
+        if (a[k] != b[k]) return a[k] < b[k] ? -1 : 1;
+    }
+    return 0;
+}
+
+static int next_perm(int *a, int m)      /* next lexicographic permutation of a[1..m-1] */
+{
+    int i = m - 2, j, t;
+    while (i >= 1 && a[i] >= a[i + 1]) i--;
+    if (i < 1) return 0;
+    j = m - 1;
+    while (a[j] <= a[i]) j--;
+    t = a[i]; a[i] = a[j]; a[j] = t;
+    for (i = i + 1, j = m - 1; i < j; i++, j--) { t = a[i]; a[i] = a[j]; a[j] = t; }
+    return 1;
+}
+
+/* Alg. 5: 0 if some image is lexicographically smaller than g (g is
+ * not the canonic form), else the number of distinct images (the power of its
+ * class).  g must be normalised (row 0 = 0..N-1).  vs != 0: the vertical mirror
+ * is left out (it is neutralised by vertical symmetry). */
+long long oracle_canonize(int n, int vs, const int *g)
+{
+    int h = n / 2, pi[MAXN], swap, mirror, k;
+    int (*imgs)[MAXN * MAXN];
+    long long count = 0, distinct = 0, cap = 2LL << 5;
+    {
+        long long f = 1;
+        for (k = 2; k < h; k++) f *= k;
+        cap = 2LL * (1LL << h) * f;
+    }
+    imgs = malloc(sizeof(*imgs) * (size_t)cap);
+    for (k = 0; k < h; k++) pi[k] = k;
+    do {
+        for (swap = 0; swap < (1 << h); swap++)
+            for (mirror = 0; mirror < (vs ? 1 : 2); mirror++) {
+                int t[MAXN * MAXN], c, seen = 0;
+                long long e;
+                apply_m(n, g, pi, swap, mirror, t);
+                c = lex_cmp(n, t, g);
+                if (c < 0) { free(imgs); return 0; }
+                for (e = 0; e < count && !seen; e++) seen = lex_cmp(n, t, imgs[e]) == 0;
+                if (!seen) { memcpy(imgs[count], t, sizeof(int) * n * n); count++; distinct++; }
+            }
+    } while (next_perm(pi, h));
+    free(imgs);
+    return distinct;
+}
+
+/* Alg. 6, first half: enumerate every design given by the first
+ * `depth` cells of `order` below `grid` (the hourglass designs when `order` lists
+ * the diagonals and row N-1), keep the canonic ones (Alg. 5) with their class
+ * sizes.  Returns the number of classes (reps/mult written up to cap); *n_designs
+ * receives the number of designs enumerated. */
+long long oracle_classes(int n, int vs, const int *grid, const int *order, int depth,
+                         int *reps, long long *mult, long long cap, long long *n_designs)
+{
+    oracle_state *s = (oracle_state *)malloc(sizeof(oracle_state));
+    long long classes;
+    int rc = load(s, n, vs, grid, order, depth);
+    if (rc != 0) { free(s); return rc; }
+    s->emit = reps; s->emit_cap = reps ? cap : 0; s->emit_depth = depth;
+    s->canon = 1; s->mult_out = mult;
+    fill(s, 0);
+    classes = s->classes;
+    if (n_designs) *n_designs = (long long)s->count;
+    free(s);
+    return classes;
 }

@@ -19,7 +19,7 @@ DLS_MAX_ORDER = 10
 DLS_STATS_WORDS = 8
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
-EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_count",
+EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_count",
            "dls_count_async", "dls_kernel_launches")
 
 _lib = None
@@ -53,6 +53,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_plan.restype = c_int
     lib.dls_split.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64]
     lib.dls_split.restype = c_i64
+    lib.dls_refine.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, c_int, vp, vp, c_i64]
+    lib.dls_refine.restype = c_i64
     lib.dls_count.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp, vp]
     lib.dls_count.restype = c_int
     lib.dls_count_async.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp]
@@ -92,6 +94,22 @@ def dls_split(n: int, depth: int, symmetric: bool = False, fixed_first_row: bool
     got = lib.dls_split(n, int(symmetric), int(fixed_first_row), depth, out.ctypes.data, total)
     _check(got, "dls_split")
     return out[:total]
+
+
+def dls_refine(n: int, depth: int, records: np.ndarray, depth2: int, symmetric: bool = False,
+               fixed_first_row: bool = True):
+    """Children of depth-`depth` records at depth2 -> (records (k, n, n) uint8, parent (k,) uint32)."""
+    lib = load()
+    recs = np.ascontiguousarray(records, dtype=np.uint8)
+    total = lib.dls_refine(n, int(symmetric), int(fixed_first_row), depth, recs.ctypes.data, len(recs), depth2,
+                           None, None, 0)
+    _check(total, "dls_refine")
+    out = np.empty((max(total, 1), n, n), dtype=np.uint8)
+    par = np.empty(max(total, 1), dtype=np.uint32)
+    got = lib.dls_refine(n, int(symmetric), int(fixed_first_row), depth, recs.ctypes.data, len(recs), depth2,
+                         out.ctypes.data, par.ctypes.data, total)
+    _check(got, "dls_refine")
+    return out[:total], par[:total]
 
 
 def _ptr(a) -> Tuple[int, object]:

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -44,11 +45,13 @@ typedef unsigned long long u64;
 
 constexpr int kMaxLevels = 100;     // n*n for n = 10
 constexpr int kBurst = 32;          // DFS steps between warp scheduling points
-constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this
+constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Device-wide donation pool (global memory, one per launch): control words
 // [0] active warps, [1] waiting warps, [2] head (claimed), [3] tail (reserved),
 // [4] warps registered (exit is allowed only once all warps of the grid are),
+// [5] slots released (read completely; producers bound tail - released so a
+//     claimed slot is never overwritten before its reader is done),
 // then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1 = pid,
 // w3 = split level | untried siblings << 16, w4.. = the values (bit indices) of
 // levels 1..split-1, 4 bits each.
@@ -369,6 +372,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
 
     uint32_t *const pool = p.pool;
     const uint32_t total_warps = gridDim.x * (uint32_t)(NT / 32);
+    const int min_donate = max(kMinDonateDepth, L / 3);   // smallest donated subtree (levels)
     if (lane == 0) {
         atomicAdd(pool + 0, 1u);                   // this warp is active
         __threadfence();
@@ -484,16 +488,21 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         S[(l + 1) * kBlock] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
                     adopt = true;
                 }
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence();
+                    atomicAdd(pool + 5, got);   // our slots may be reused from now on
+                }
             } else {
                 // shallowest open level of each busy lane (its untried siblings)
                 int dsplit = 0;
                 uint32_t drest = 0;
                 if (pid >= 0 && lvl > 0) {
-                    for (int l = 1; l < lvl && l <= L - kMinDonateDepth; ++l) {
+                    for (int l = 1; l < lvl && l <= L - min_donate; ++l) {
                         const uint32_t s = S[(l + 1) * kBlock];
                         if (s & (s - 1u)) { dsplit = l; drest = s & (s - 1u); break; }
                     }
-                    if (!dsplit && lvl <= L - kMinDonateDepth && (cur & (cur - 1u))) {
+                    if (!dsplit && lvl <= L - min_donate && (cur & (cur - 1u))) {
                         dsplit = lvl;
                         drest = cur & (cur - 1u);   // keep the lowest for ourselves
                     }
@@ -536,13 +545,16 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     // ---- donors left over: feed the device-wide pool if a warp waits
                     uint32_t feed = 0;
                     if (lane == 0)
-                        feed = (ld_acquire(pool + 1) != 0u && (int)(ld_acquire(pool + 3) - ld_acquire(pool + 2)) < (int)kPoolLimit) ? 1u : 0u;
+                        feed = (ld_acquire(pool + 1) != 0u && (int)(ld_acquire(pool + 3) - ld_acquire(pool + 5)) < (int)kPoolLimit) ? 1u : 0u;
                     feed = __shfl_sync(kFull, feed, 0);
                     if (feed) {
                         // the lane with the shallowest open level donates it
-                        const uint32_t key = dsplit > 0 ? ((uint32_t)dsplit << 5) | (uint32_t)lane : 0xFFFFFFFFu;
+                        // (only subtrees from the upper half of the tree are worth a trip
+                        // through global memory)
+                        const uint32_t key = (dsplit > 0 && 2 * dsplit <= L) ? ((uint32_t)dsplit << 5) | (uint32_t)lane
+                                                                             : 0xFFFFFFFFu;
                         const uint32_t best = __reduce_min_sync(kFull, key);
-                        if ((best & 31u) == (uint32_t)lane) {
+                        if (best != 0xFFFFFFFFu && (best & 31u) == (uint32_t)lane) {
                             const uint32_t ticket = atomicAdd(pool + 3, 1u);
                             uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
                             slot[1] = (uint32_t)pid;
@@ -650,6 +662,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         atomicAdd(p.stats + 4, a[2]);   // donations
         atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
         atomicAdd(p.stats + 6, a[4]);   // lane-bursts
+        atomicMax(p.stats + 7, (u64)ld_acquire(pool + 3));   // subtrees published to the pool
     }
 }
 
@@ -763,6 +776,7 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
         if (symmetric) set((c / n) * n + (n - 1 - c % n));
     }
     prm->donate = 1;
+    if (const char *e = getenv("DLS_DONATE")) prm->donate = atoi(e);   // 0: no donation (diagnostics)
     return DLS_OK;
 }
 

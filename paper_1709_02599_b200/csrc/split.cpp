@@ -206,3 +206,23 @@ extern "C" int64_t dls_split(int n, int symmetric, int fixed_first_row, int dept
         for (int j = 0; j < n; ++j) root[j] = (uint8_t)j;
     return dls::refine(plan, 0, depth, root, 1, out_prefixes, nullptr, capacity, nullptr);
 }
+
+extern "C" int64_t dls_refine(int n, int symmetric, int fixed_first_row, int depth, const uint8_t *in,
+                              int64_t n_in, int depth2, uint8_t *out, uint32_t *parent, int64_t capacity) {
+    dls::Plan plan;
+    if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
+        dls::set_error("dls_refine: unsupported (n, symmetric, fixed_first_row)");
+        return DLS_E_ARG;
+    }
+    if (depth < 0 || depth2 < depth || depth2 > (int)plan.cells.size() || n_in < 0 || (n_in > 0 && !in) ||
+        capacity < 0 || (capacity > 0 && !out)) {
+        dls::set_error("dls_refine: bad depth / sizes");
+        return DLS_E_ARG;
+    }
+    for (int64_t p = 0; p < n_in; ++p)
+        if (!dls::valid_record(plan, depth, in + p * n * n)) {
+            dls::set_error("dls_refine: record is not a consistent depth-d prefix");
+            return DLS_E_PREFIX;
+        }
+    return dls::refine(plan, depth, depth2, in, n_in, out, parent, capacity, nullptr);
+}
