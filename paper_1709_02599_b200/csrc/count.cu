@@ -30,6 +30,7 @@
 //    (optional) and one 64-bit atomicAdd per block for the total.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -77,6 +78,8 @@ struct Params {
     u64 pat[2];              // cells assigned in a prefix, bit i*n+j
     int L;                   // number of searched levels (plan cells after the prefix)
     int donate;              // enable warp-level subtree donation
+    int min_donate;          // smallest donated subtree (levels below the split)
+    uint32_t total_warps;    // warps of the grid (exit once all registered)
     Tab tab[kMaxLevels + 2]; // tab[t + 1], t = -1 .. L
 };
 
@@ -371,8 +374,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const char *const Cb = reinterpret_cast<const char *>(Cl);
 
     uint32_t *const pool = p.pool;
-    const uint32_t total_warps = gridDim.x * (uint32_t)(NT / 32);
-    const int min_donate = max(kMinDonateDepth, L / 3);   // smallest donated subtree (levels)
+
     if (lane == 0) {
         atomicAdd(pool + 0, 1u);                   // this warp is active
         __threadfence();
@@ -458,7 +460,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                         __threadfence();
                         const uint32_t a = ld_acquire(pool + 0);
                         __threadfence();
-                        done = (reg == total_warps && a == 0u && ld_acquire(pool + 2) == ld_acquire(pool + 3)) ? 1u : 0u;
+                        done = (reg == p.total_warps && a == 0u && ld_acquire(pool + 2) == ld_acquire(pool + 3)) ? 1u : 0u;
                     }
                 }
                 got = __shfl_sync(kFull, got, 0);
@@ -498,11 +500,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 int dsplit = 0;
                 uint32_t drest = 0;
                 if (pid >= 0 && lvl > 0) {
-                    for (int l = 1; l < lvl && l <= L - min_donate; ++l) {
+                    for (int l = 1; l < lvl && l <= L - p.min_donate; ++l) {
                         const uint32_t s = S[(l + 1) * kBlock];
                         if (s & (s - 1u)) { dsplit = l; drest = s & (s - 1u); break; }
                     }
-                    if (!dsplit && lvl <= L - min_donate && (cur & (cur - 1u))) {
+                    if (!dsplit && lvl <= L - p.min_donate && (cur & (cur - 1u))) {
                         dsplit = lvl;
                         drest = cur & (cur - 1u);   // keep the lowest for ourselves
                     }
@@ -776,6 +778,7 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
         if (symmetric) set((c / n) * n + (n - 1 - c % n));
     }
     prm->donate = 1;
+    prm->min_donate = std::max(kMinDonateDepth, prm->L / 3);
     if (const char *e = getenv("DLS_DONATE")) prm->donate = atoi(e);   // 0: no donation (diagnostics)
     return DLS_OK;
 }
@@ -811,6 +814,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     if ((e = cudaMemsetAsync(pool, 0, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(pool)");
     Params q = prm;
     q.pool = (uint32_t *)pool;
+    q.total_warps = (uint32_t)sms * (uint32_t)(nthreads / 32);
     fn<<<(unsigned)sms, nthreads, smem, stream>>>(q);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "kernel launch");
     if ((e = cudaFreeAsync(pool, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(pool)");
