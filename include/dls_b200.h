@@ -140,6 +140,33 @@ int dls_count_async(int n, int symmetric, int fixed_first_row, int depth,
                     uint64_t *d_counts, uint64_t *d_stats, void *stream);
 
 /*
+ * dls_canonize -- Alg. 5 on the GPU for hourglass designs (row 0 =
+ * 0..n-1, both diagonals and row n-1 assigned): out_mult[i] = 0 if record
+ * i is not the lexicographically smallest design of its class under the
+ * M-transformations that keep hourglass designs, else the number of
+ * designs in its class.  The group: symmetric pairs of rows+columns permuted with
+ * pair {0, n-1} in place, each pair optionally swapped, columns optionally
+ * mirrored (the mirror is left out when symmetric: P:524).  3 <= n <= 10.
+ *   hourglasses    n_rec records (host or device); out_mult n_rec uint32 (host or device).
+ */
+int dls_canonize(int n, int symmetric, const uint8_t *hourglasses, int64_t n_rec,
+                 uint32_t *out_mult, void *stream);
+
+/*
+ * dls_count_sb -- the symmetry-broken enumeration of Alg. 6 for the
+ * first-row-fixed problem: every hourglass design is generated and canonised on
+ * the GPU, the completions of each canonic design are counted by the search
+ * kernel (plan: diagonals, row n-1, then Section 2.3) and multiplied by its class
+ * size (Corollary 1).
+ *   out_total       host: number of (vertically symmetric) DLS, first row fixed;
+ *   out_hourglasses host: hourglass designs generated; out_classes: canonic ones;
+ *   out_nodes       host: search nodes below the canonic designs.
+ * Synchronous.  3 <= n <= 10 (even when symmetric).
+ */
+int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t *out_hourglasses,
+                 uint64_t *out_classes, uint64_t *out_nodes, void *stream);
+
+/*
  * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
  * per call (for the bench's launch count): the search kernel only.
  */

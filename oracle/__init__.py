@@ -62,6 +62,8 @@ def _load():
         lib.oracle_plan.restype = ctypes.c_int
         lib.oracle_canonize.argtypes = [ctypes.c_int, ctypes.c_int, ip]
         lib.oracle_canonize.restype = ctypes.c_longlong
+        lib.oracle_transform.argtypes = [ctypes.c_int, ip, ip, ctypes.c_int, ctypes.c_int, ip]
+        lib.oracle_transform.restype = None
         llp = ctypes.POINTER(ctypes.c_longlong)
         lib.oracle_classes.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ip, llp,
                                        ctypes.c_longlong, llp]
@@ -287,7 +289,8 @@ def canonize(n: int, vs: bool, grid: np.ndarray) -> int:
 
 def hourglass_classes(n: int, vs: bool = False, keep: bool = True):
     """Canonic hourglass designs and their class sizes (Alg. 5/6).
-    Returns (reps (k, n, n) int32 or None, mult (k,) int64 or None, n_hourglasses)."""
+    Returns (reps (k, n, n) int32, mult (k,) int64, n_hourglasses), or with
+    keep=False (number of classes, None, n_hourglasses) from a single pass."""
     lib = _load()
     cells = hourglass_cells(n)
     if vs:
@@ -300,9 +303,26 @@ def hourglass_classes(n: int, vs: bool = False, keep: bool = True):
     if k < 0:
         raise ValueError("oracle_classes failed: %d" % k)
     if not keep:
-        return None, None, int(nd.value)
+        return int(k), None, int(nd.value)
     reps = np.zeros((max(k, 1), n * n), dtype=np.int32)
     mult = np.zeros(max(k, 1), dtype=np.int64)
     lib.oracle_classes(n, int(bool(vs)), gp, op, len(cells), reps.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
                        mult.ctypes.data_as(llp), k, ctypes.byref(nd))
     return reps[:k].reshape(-1, n, n), mult[:k], int(nd.value)
+
+
+def transform(n: int, grid: np.ndarray, pi: Sequence[int], swap: int, mirror: bool) -> np.ndarray:
+    """Image of a (partial) square under one M-transformation, renamed so that row
+    0 reads 0..N-1."""
+    g, gp = _iarr(np.asarray(grid).reshape(-1))
+    p_, pp = _iarr(list(pi))
+    out = np.zeros(n * n, dtype=np.int32)
+    _load().oracle_transform(n, gp, pp, int(swap), int(bool(mirror)), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+    return out.reshape(n, n)
+
+
+def group_size(n: int, vs: bool = False) -> int:
+    """2 * 2^h * (h-1)! transformations keep hourglass designs (Alg. 5 loop bounds,
+    P:404-406); the mirror is neutralised for VS squares."""
+    h = n // 2
+    return (1 if vs else 2) * (2 ** h) * math.factorial(h - 1)

@@ -406,3 +406,10 @@ long long oracle_classes(int n, int vs, const int *grid, const int *order, int d
     free(s);
     return classes;
 }
+
+/* One M-transformation (see apply_m) of a design, exported for the Proposition 1
+ * tests: pi = permutation of the h pairs (pi[0] = 0), swap = subset of pairs. */
+void oracle_transform(int n, const int *g, const int *pi, int swap, int mirror, int *out)
+{
+    apply_m(n, g, pi, swap, mirror, out);
+}

@@ -20,7 +20,7 @@ DLS_STATS_WORDS = 8
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_count",
-           "dls_count_async", "dls_kernel_launches")
+           "dls_count_async", "dls_canonize", "dls_count_sb", "dls_kernel_launches")
 
 _lib = None
 
@@ -59,6 +59,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_count.restype = c_int
     lib.dls_count_async.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp]
     lib.dls_count_async.restype = c_int
+    lib.dls_canonize.argtypes = [c_int, c_int, vp, c_i64, vp, vp]
+    lib.dls_canonize.restype = c_int
+    lib.dls_count_sb.argtypes = [c_int, c_int, vp, vp, vp, vp, vp]
+    lib.dls_count_sb.restype = c_int
     lib.dls_kernel_launches.restype = c_int
     _lib = lib
     return lib
@@ -155,6 +159,25 @@ def dls_count_async(n: int, depth: int, d_prefixes, d_counts, d_stats, symmetric
     rc = load().dls_count_async(n, int(symmetric), int(fixed_first_row), depth, pp or None,
                                 int(d_prefixes.shape[0]), cp or None, sp, stream or None)
     _check(rc, "dls_count_async")
+
+
+def dls_canonize(n: int, hourglasses, symmetric: bool = False, stream: Optional[int] = None) -> np.ndarray:
+    """Alg. 5 on the GPU: class size of every canonic hourglass record, 0 otherwise."""
+    recs = hourglasses
+    k = int(recs.shape[0])
+    out = np.zeros(max(k, 1), dtype=np.uint32)
+    pp, keep = _ptr(recs)
+    rc = load().dls_canonize(n, int(symmetric), pp or None, k, out.ctypes.data, stream or None)
+    _check(rc, "dls_canonize")
+    return out[:k]
+
+
+def dls_count_sb(n: int, symmetric: bool = False, stream: Optional[int] = None) -> dict:
+    """Alg. 6 on the GPU -> {count, hourglasses, classes, nodes} (first row fixed)."""
+    vals = [ctypes.c_uint64(0) for _ in range(4)]
+    rc = load().dls_count_sb(n, int(symmetric), *[ctypes.addressof(v) for v in vals], stream or None)
+    _check(rc, "dls_count_sb")
+    return {"count": vals[0].value, "hourglasses": vals[1].value, "classes": vals[2].value, "nodes": vals[3].value}
 
 
 def dls_kernel_launches() -> int:

@@ -752,13 +752,10 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
     }
 }
 
-// Everything a launch needs that depends only on (n, vs, fixed_first_row, depth).
-int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
-    dls::Plan plan;
-    if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
-        dls::set_error("dls_count: unsupported (n, symmetric, fixed_first_row)");
-        return DLS_E_ARG;
-    }
+// Everything a launch needs that depends only on (plan, depth).
+int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
+    const int n = plan.n;
+    const bool symmetric = plan.vs;
     const int steps = (int)plan.cells.size();
     if (depth < plan.diag_depth || depth > steps) {
         dls::set_error("dls_count: depth must satisfy diag_depth <= depth <= n_steps");
@@ -770,8 +767,8 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
     fill_tab(n, symmetric, level_cells, prm->tab);
     // assigned-cell pattern of a depth-`depth` prefix
     auto set = [&](int c) { prm->pat[c >> 6] |= 1ull << (c & 63); };
-    if (fixed_first_row)
-        for (int j = 0; j < n; ++j) set(j);
+    for (int c = 0; c < n * n; ++c)
+        if (plan.pre[c]) set(c);
     for (int s = 0; s < depth; ++s) {
         const int c = plan.cells[s];
         set(c);
@@ -781,6 +778,15 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
     prm->min_donate = std::max(kMinDonateDepth, prm->L / 3);
     if (const char *e = getenv("DLS_DONATE")) prm->donate = atoi(e);   // 0: no donation (diagnostics)
     return DLS_OK;
+}
+
+int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
+    dls::Plan plan;
+    if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
+        dls::set_error("dls_count: unsupported (n, symmetric, fixed_first_row)");
+        return DLS_E_ARG;
+    }
+    return prepare_plan(plan, depth, prm);
 }
 
 size_t smem_bytes(int n, bool vs, int L, int nthreads) {
@@ -892,19 +898,22 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
 
-extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
-                         const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
-                         uint64_t *out_total, uint64_t *out_nodes, void *stream) {
+
+namespace dls {
+
+// dls_count for an arbitrary plan (the standard one, or the hourglass plan of
+// the symmetry-broken driver).
+int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
+                  uint64_t *out_total, uint64_t *out_nodes, void *stream) {
     int rc = have_device();
     if (rc) return rc;
     if (n_prefix < 0 || n_prefix >= (int64_t)1 << 31 || (n_prefix > 0 && !prefix_buf)) {
         dls::set_error("dls_count: bad pointers / sizes");
         return DLS_E_ARG;
     }
-    dls::Plan plan;
+    const int n = plan.n;
     Params prm;
-    if ((rc = prepare(n, symmetric, fixed_first_row, depth, &prm))) return rc;
-    dls::make_plan(n, symmetric, fixed_first_row, &plan);
+    if ((rc = prepare_plan(plan, depth, &prm))) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const int nn = n * n;
     const int steps = (int)plan.cells.size();
@@ -939,7 +948,7 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
         h_sub.resize((size_t)cnt * nn + 1);
         h_parent.resize((size_t)cnt + 1);
         dls::refine(plan, depth, d1, src, n_prefix, h_sub.data(), h_parent.data(), cnt, &extra_nodes);
-        if ((rc = prepare(n, symmetric, fixed_first_row, d1, &prm))) return rc;
+        if ((rc = prepare_plan(plan, d1, &prm))) return rc;
         src = h_sub.data();
         n_rec = cnt;
         depth_run = d1;
@@ -986,7 +995,7 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
         prm.counts = d_counts;
         prm.parent = refined ? (const uint32_t *)(base + off_par) : nullptr;
         prm.stats = d_stats;
-        if ((rc = launch(n, symmetric, prm, s))) { cudaStreamSynchronize(s); return rc; }
+        if ((rc = launch(n, plan.vs, prm, s))) { cudaStreamSynchronize(s); return rc; }
     }
     u64 stats[DLS_STATS_WORDS];
     if ((e = cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
@@ -1002,4 +1011,17 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
         return DLS_E_PREFIX;
     }
     return DLS_OK;
+}
+
+}  // namespace dls
+
+extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
+                         const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
+                         uint64_t *out_total, uint64_t *out_nodes, void *stream) {
+    dls::Plan plan;
+    if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
+        dls::set_error("dls_count: unsupported (n, symmetric, fixed_first_row)");
+        return DLS_E_ARG;
+    }
+    return dls::count_records(plan, depth, prefix_buf, n_prefix, out_counts, out_total, out_nodes, stream);
 }

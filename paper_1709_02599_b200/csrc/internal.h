@@ -17,10 +17,20 @@ struct Plan {
     std::vector<int> cells;      // i*n+j in fill order
     std::vector<uint8_t> forced; // 1 = taken by the forced-cell rule
     int diag_depth = 0;          // first depth covering both diagonals
+    int hourglass_depth = 0;     // hourglass plans: depth covering row N-1 too
+    std::vector<uint8_t> pre;    // n*n, 1 = assigned a priori (not planned)
 };
 
 // Returns false on bad arguments.
 bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out);
+
+// Section 2.3 order below an arbitrary a-priori pattern `pre` (n*n), taking the
+// cells of `head` first (in that order) and then the V-score / forced rule.
+bool make_plan_from(int n, bool vs, const uint8_t *pre, const std::vector<int> &head, Plan *out);
+
+// Hourglass plan (Section 4.3): row 0 fixed, the diagonal cells in the
+// standard order, then the cells of row N-1, then the rule of Section 2.3.
+bool make_hourglass_plan(int n, bool vs, Plan *out);
 
 // Validity of (n, symmetric) combinations.
 bool valid_problem(int n, int symmetric, int fixed_first_row);
@@ -33,6 +43,10 @@ int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in
 
 // Host-side check that a record is a consistent depth-`depth` prefix of `plan`.
 bool valid_record(const Plan &plan, int depth, const uint8_t *rec);
+
+// dls_count for an arbitrary plan (count.cu).
+int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
+                  uint64_t *out_total, uint64_t *out_nodes, void *stream);
 
 void set_error(const std::string &msg);
 const char *get_error();

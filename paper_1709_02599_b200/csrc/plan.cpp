@@ -33,28 +33,42 @@ bool valid_problem(int n, int symmetric, int fixed_first_row) {
     return true;
 }
 
-bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out) {
-    if (!valid_problem(n, vs, fixed_first_row)) return false;
+bool make_plan_from(int n, bool vs, const uint8_t *pre, const std::vector<int> &head, Plan *out) {
+    if (n < 1 || n > DLS_MAX_ORDER || (vs && (n % 2) != 0)) return false;
     Plan p;
     p.n = n;
     p.vs = vs;
-    p.fixed_first_row = fixed_first_row;
+    p.pre.assign(pre, pre + n * n);
+    p.fixed_first_row = true;
+    for (int j = 0; j < n; ++j) p.fixed_first_row = p.fixed_first_row && pre[j];
 
     bool taken[DLS_MAX_ORDER][DLS_MAX_ORDER] = {};
     int in_row[DLS_MAX_ORDER] = {}, in_col[DLS_MAX_ORDER] = {};
     int in_md = 0, in_ad = 0;
+    int assigned = 0;
     auto take = [&](int i, int j) {
+        if (taken[i][j]) return;
         taken[i][j] = true;
         in_row[i]++;
         in_col[j]++;
         if (i == j) in_md++;
         if (i + j == n - 1) in_ad++;
+        assigned++;
     };
-    if (fixed_first_row)
-        for (int j = 0; j < n; ++j) take(0, j);
-
-    const int total = n * n - (fixed_first_row ? n : 0);
-    int assigned = 0;
+    for (int c = 0; c < n * n; ++c)
+        if (pre[c]) take(c / n, c % n);
+    const int pre_count = assigned;
+    // cells the caller wants first (e.g. a hourglass: diagonals, then row N-1)
+    for (int c : head) {
+        int i = c / n, j = c % n;
+        if (vs && 2 * j > n - 1) j = n - 1 - j;
+        if (taken[i][j]) continue;
+        take(i, j);
+        if (vs) take(i, n - 1 - j);
+        p.cells.push_back(i * n + j);
+        p.forced.push_back(0);
+    }
+    const int total = n * n;
     while (assigned < total) {
         int pi = -1, pj = -1;
         bool forced = false;
@@ -87,21 +101,19 @@ bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out) {
         if (pi < 0) break;
         if (vs && 2 * pj > n - 1) pj = n - 1 - pj;  // plan the left-half representative
         take(pi, pj);
-        assigned++;
-        if (vs && pj != n - 1 - pj) { take(pi, n - 1 - pj); assigned++; }
+        if (vs && pj != n - 1 - pj) take(pi, n - 1 - pj);
         p.cells.push_back(pi * n + pj);
         p.forced.push_back(forced ? 1 : 0);
     }
+    (void)pre_count;
 
     // diag depth: first prefix length after which every diagonal cell is assigned
     int remaining = 0;
     bool diag_cell[DLS_MAX_ORDER][DLS_MAX_ORDER] = {};
-    for (int k = 0; k < n; ++k) {
-        diag_cell[k][k] = diag_cell[k][n - 1 - k] = true;
-    }
+    for (int k = 0; k < n; ++k) diag_cell[k][k] = diag_cell[k][n - 1 - k] = true;
     bool done[DLS_MAX_ORDER][DLS_MAX_ORDER] = {};
-    if (fixed_first_row)
-        for (int j = 0; j < n; ++j) done[0][j] = true;
+    for (int c = 0; c < n * n; ++c)
+        if (pre[c]) done[c / n][c % n] = true;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j)
             if (diag_cell[i][j] && !done[i][j]) remaining++;
@@ -115,6 +127,37 @@ bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out) {
         p.diag_depth = (int)s + 1;
     }
     *out = std::move(p);
+    return true;
+}
+
+bool make_plan(int n, bool vs, bool fixed_first_row, Plan *out) {
+    if (!valid_problem(n, vs, fixed_first_row)) return false;
+    uint8_t pre[DLS_MAX_ORDER * DLS_MAX_ORDER] = {};
+    if (fixed_first_row)
+        for (int j = 0; j < n; ++j) pre[j] = 1;
+    return make_plan_from(n, vs, pre, {}, out);
+}
+
+bool make_hourglass_plan(int n, bool vs, Plan *out) {
+    // Section 4.3: "the first row is fixed beforehand, and the diagonals are
+    // filled before everything else. Thus to produce hourglass designs we need only
+    // to fill the last row of cells right after filling diagonals."
+    Plan base;
+    if (!make_plan(n, vs, true, &base)) return false;
+    std::vector<int> head(base.cells.begin(), base.cells.begin() + base.diag_depth);
+    for (int j = 0; j < n; ++j) head.push_back((n - 1) * n + j);
+    uint8_t pre[DLS_MAX_ORDER * DLS_MAX_ORDER] = {};
+    for (int j = 0; j < n; ++j) pre[j] = 1;
+    if (!make_plan_from(n, vs, pre, head, out)) return false;
+    // number of head cells actually planned (row N-1 minus its diagonal cells)
+    int k = 0;
+    for (int c : out->cells) {
+        bool in_head = false;
+        for (int h : head) in_head = in_head || h == c;
+        if (!in_head) break;
+        ++k;
+    }
+    out->hourglass_depth = k;
     return true;
 }
 

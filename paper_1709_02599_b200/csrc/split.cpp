@@ -168,8 +168,7 @@ int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in
 bool valid_record(const Plan &plan, int depth, const uint8_t *rec) {
     const int n = plan.n;
     bool want[DLS_MAX_ORDER * DLS_MAX_ORDER] = {};
-    if (plan.fixed_first_row)
-        for (int j = 0; j < n; ++j) want[j] = true;
+    for (int c = 0; c < n * n; ++c) want[c] = plan.pre[c] != 0;
     for (int s = 0; s < depth; ++s) {
         const int c = plan.cells[s];
         want[c] = true;
