@@ -167,6 +167,16 @@ int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t *out_hourgl
                  uint64_t *out_classes, uint64_t *out_nodes, void *stream);
 
 /*
+ * dls_count_sb_range -- the same over the diagonal workunits [diag_begin,
+ * diag_end) of dls_split(n, symmetric, 1, diag depth) (diag_end < 0: to the end),
+ * so that long runs (e.g. n = 9) can be split and resumed; the totals of all
+ * ranges add up to dls_count_sb's.
+ */
+int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int64_t diag_end,
+                       uint64_t *out_total, uint64_t *out_hourglasses, uint64_t *out_classes,
+                       uint64_t *out_nodes, void *stream);
+
+/*
  * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
  * per call (for the bench's launch count): the search kernel only.
  */

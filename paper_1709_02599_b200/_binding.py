@@ -20,7 +20,7 @@ DLS_STATS_WORDS = 8
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_count",
-           "dls_count_async", "dls_canonize", "dls_count_sb", "dls_kernel_launches")
+           "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_kernel_launches")
 
 _lib = None
 
@@ -63,6 +63,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_canonize.restype = c_int
     lib.dls_count_sb.argtypes = [c_int, c_int, vp, vp, vp, vp, vp]
     lib.dls_count_sb.restype = c_int
+    lib.dls_count_sb_range.argtypes = [c_int, c_int, c_i64, c_i64, vp, vp, vp, vp, vp]
+    lib.dls_count_sb_range.restype = c_int
     lib.dls_kernel_launches.restype = c_int
     _lib = lib
     return lib
@@ -177,6 +179,14 @@ def dls_count_sb(n: int, symmetric: bool = False, stream: Optional[int] = None) 
     vals = [ctypes.c_uint64(0) for _ in range(4)]
     rc = load().dls_count_sb(n, int(symmetric), *[ctypes.addressof(v) for v in vals], stream or None)
     _check(rc, "dls_count_sb")
+    return {"count": vals[0].value, "hourglasses": vals[1].value, "classes": vals[2].value, "nodes": vals[3].value}
+
+
+def dls_count_sb_range(n: int, begin: int, end: int, symmetric: bool = False, stream: Optional[int] = None) -> dict:
+    """Alg. 6 over the diagonal workunits [begin, end) (end < 0: to the end)."""
+    vals = [ctypes.c_uint64(0) for _ in range(4)]
+    rc = load().dls_count_sb_range(n, int(symmetric), begin, end, *[ctypes.addressof(v) for v in vals], stream or None)
+    _check(rc, "dls_count_sb_range")
     return {"count": vals[0].value, "hourglasses": vals[1].value, "classes": vals[2].value, "nodes": vals[3].value}
 
 

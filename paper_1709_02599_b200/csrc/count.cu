@@ -36,6 +36,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -334,10 +335,13 @@ struct Layout {
     static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT != 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
     static constexpr int CTW = BYTES ? 2 : 4;                 // words of a read entry
     static constexpr int BLK_WORDS = 32 * (4 + CTW);          // words per transition block
+    // stack entries: N <= 16 bit candidate sets; u16 for the 64-bit layout (N = 9,
+    // 10 DLS: long searches, so the smaller stack buys 1024 lanes per SM), else u32
+    typedef typename std::conditional<Geo<N, VS>::LAYOUT == 2, uint16_t, uint32_t>::type SW;
 };
 
 template <int N, bool VS>
-__global__ void __launch_bounds__(Geo<N, VS>::LAYOUT != 2 ? 1024 : 512, 1)
+__global__ void __launch_bounds__(1024, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
@@ -348,7 +352,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    uint32_t *const stack = smem + (L + 2) * LY::BLK_WORDS;
+    typedef typename LY::SW SW;
+    SW *const stack = reinterpret_cast<SW *>(smem + (L + 2) * LY::BLK_WORDS);
 
     for (int k = tid; k < (L + 2) * 32; k += NT) {
         const Tab &e = p.tab[k >> 5];
@@ -363,7 +368,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     stack[NT + tid] = 0u;
     __syncthreads();
     // slot of level l (l = -1 .. L): S[(l + 1) * NT]
-    uint32_t *const S = stack + tid;
+    SW *const S = stack + tid;
     // transition t: Fl[t * kBlk] (toggle part), Cl[t * kBlkC] (read part)
     constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
     constexpr int kBlkC = LY::BLK_WORDS / LY::CTW;           // block stride in CT units
@@ -525,7 +530,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     const bool give = dsplit > 0 && dn_rank < pairs;
                     if (recv) {
                         // copy the donor's path above the split level
-                        const uint32_t *const Sd = stack + (tid - lane + src);
+                        const SW *const Sd = stack + (tid - lane + src);
                         for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
                     }
                     __syncwarp();
@@ -615,7 +620,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const bool dn = cur != 0u;                     // descend: cell(lvl) has candidates
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
             const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
-            uint32_t *const sl = S + lvl * NT;             // slot of level lvl-1
+            SW *const sl = S + lvl * NT;                   // slot of level lvl-1
             const uint32_t sp = *sl;                       // its L (lowest bit = assigned value)
             const uint32_t bb = sp & (0u - sp);
             const uint32_t sibs = sp - bb;                 // L &= L-1
@@ -791,7 +796,8 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
 
 size_t smem_bytes(int n, bool vs, int L, int nthreads) {
     const size_t ct = layout_of(n, vs) == 0 ? 8 : 16;
-    return (size_t)(L + 2) * 32 * (16 + ct) + (size_t)(L + 2) * nthreads * sizeof(uint32_t);
+    const size_t sw = layout_of(n, vs) == 2 ? 2 : 4;
+    return (size_t)(L + 2) * 32 * (16 + ct) + (size_t)(L + 2) * nthreads * sw;
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
@@ -807,7 +813,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators)
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     const int lay = layout_of(n, vs);
-    int nthreads = lay != 2 ? 1024 : 512;   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
+    int nthreads = 1024;                   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
     while (lay == 2 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
     const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }

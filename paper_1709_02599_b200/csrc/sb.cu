@@ -346,8 +346,9 @@ extern "C" int dls_canonize(int n, int symmetric, const uint8_t *hourglasses, in
     return e == cudaSuccess ? DLS_OK : fail(e, "dls_canonize");
 }
 
-extern "C" int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t *out_hourglasses,
-                            uint64_t *out_classes, uint64_t *out_nodes, void *stream) {
+extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int64_t diag_end, uint64_t *out_total,
+                                  uint64_t *out_hourglasses, uint64_t *out_classes, uint64_t *out_nodes,
+                                  void *stream) {
     int dev_count = 0;
     if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
         cudaGetLastError();
@@ -373,11 +374,19 @@ extern "C" int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t 
     sp.k_last = hd - dd;
     for (int l = 0; l < sp.k_last; ++l) sp.last_cols[l] = (uint8_t)(hg.cells[dd + l] % n);
     sp.group = build_group(n, symmetric, &sp.mirror_choices);
-    // diagonal workunits (host split), processed in chunks to bound memory
-    const int64_t n_diag = dls_split(n, symmetric, 1, dd, nullptr, 0);
-    if (n_diag < 0) return (int)n_diag;
-    std::vector<uint8_t> diag((size_t)std::max<int64_t>(n_diag, 1) * nn);
-    dls_split(n, symmetric, 1, dd, diag.data(), n_diag);
+    // diagonal workunits (host split), the range [diag_begin, diag_end) of them,
+    // processed in chunks to bound memory
+    const int64_t n_all = dls_split(n, symmetric, 1, dd, nullptr, 0);
+    if (n_all < 0) return (int)n_all;
+    if (diag_end < 0 || diag_end > n_all) diag_end = n_all;
+    if (diag_begin < 0 || diag_begin > diag_end) {
+        dls::set_error("dls_count_sb_range: bad range");
+        return DLS_E_ARG;
+    }
+    std::vector<uint8_t> all((size_t)std::max<int64_t>(n_all, 1) * nn);
+    dls_split(n, symmetric, 1, dd, all.data(), n_all);
+    const int64_t n_diag = diag_end - diag_begin;
+    const uint8_t *const diag_base = all.data() + diag_begin * nn;
     const int64_t chunk = 1 << 20;
     const long long cap = 1 << 22;     // canonic hourglasses per chunk
     uint8_t *d_diag = nullptr, *d_rec = nullptr;
@@ -403,7 +412,7 @@ extern "C" int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t 
     std::vector<uint64_t> counts;
     for (int64_t off = 0; off < n_diag; off += chunk) {
         const int64_t m = std::min<int64_t>(chunk, n_diag - off);
-        cudaMemcpyAsync(d_diag, diag.data() + off * nn, (size_t)m * nn, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_diag, diag_base + off * nn, (size_t)m * nn, cudaMemcpyHostToDevice, s);
         cudaMemsetAsync(d_cnt, 0, 4 * sizeof(unsigned long long), s);
         sp.diag = d_diag;
         sp.n_diag = m;
@@ -438,4 +447,9 @@ extern "C" int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t 
     if (out_classes) *out_classes = classes;
     if (out_nodes) *out_nodes = nodes;
     return DLS_OK;
+}
+
+extern "C" int dls_count_sb(int n, int symmetric, uint64_t *out_total, uint64_t *out_hourglasses,
+                            uint64_t *out_classes, uint64_t *out_nodes, void *stream) {
+    return dls_count_sb_range(n, symmetric, 0, -1, out_total, out_hourglasses, out_classes, out_nodes, stream);
 }

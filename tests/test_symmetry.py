@@ -167,3 +167,14 @@ def test_gpu_count_sb_vs10_paper():
     """82 731 715 264 512 vertically symmetric DLS of order 10 (row 0 fixed)."""
     r = D.dls_count_sb(10, True)
     assert r["count"] == paper_counts()["vsdls10_first_row_fixed"]
+
+
+@pytest.mark.gpu
+def test_gpu_count_sb_ranges_add_up():
+    n = 7
+    full = D.dls_count_sb(n)
+    total = D.load().dls_split(n, 0, 1, D.default_split_depth(n), None, 0)
+    cuts = [0, 5, total // 3, total - 1, total]
+    parts = [D.dls_count_sb_range(n, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    for key in ("count", "hourglasses", "classes"):
+        assert sum(p[key] for p in parts) == full[key]
