@@ -315,6 +315,12 @@ def main():
         peak = int_issue_peak_tops(sm_mhz)
         per_launch_ms = local_ms / args.steps
         achieved = nodes_l[0] / world * OPS_PER_NODE / (per_launch_ms / 1e3) / 1e12
+        ncu = {}
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_ncu_final.json")) as f:
+                ncu = json.load(f)
+        except (OSError, ValueError):
+            pass
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -326,7 +332,12 @@ def main():
                        "parallelism": "workunits round-robin over %d rank(s)" % world},
             "nodes_per_sec": nodes_per_sec,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": (ncu["dram_read_bytes"] + ncu["dram_write_bytes"]) if ncu else None,
+                         "traffic_note": "DRAM bytes per launch from the committed ncu --set full capture "
+                                         "(profiles/r1_ncu_final.json) = the 35 MB of workunit records: the "
+                                         "search itself never touches HBM",
+                         "issue_slots_busy_ncu": (ncu.get("issue_slots_busy_pct", 0) / 100.0) if ncu else None,
                          "note": "integer-issue roofline at %.0f MHz (MEASURED_PEAKS sm_max_mhz): 148 SMs x 4 SMSP x "
                                  "32 lanes; achieved = %d algorithmic int ops/node (Alg. 4) x nodes / kernel time"
                                  % (sm_mhz, OPS_PER_NODE)},
