@@ -910,7 +910,7 @@ namespace dls {
 // dls_count for an arbitrary plan (the standard one, or the hourglass plan of
 // the symmetry-broken driver).
 int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
-                  uint64_t *out_total, uint64_t *out_nodes, void *stream) {
+                  uint64_t *out_total, uint64_t *out_nodes, void *stream, int64_t refine_below) {
     int rc = have_device();
     if (rc) return rc;
     if (n_prefix < 0 || n_prefix >= (int64_t)1 << 31 || (n_prefix > 0 && !prefix_buf)) {
@@ -935,7 +935,8 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
     int depth_run = depth;
     int64_t extra_nodes = 0;
     bool bad_prefix = false;
-    if (n_prefix > 0 && n_prefix < kRefineTarget / 8 && depth + 1 <= steps - kMinSearchLevels) {
+    if (refine_below < 0) refine_below = kRefineTarget / 8;
+    if (n_prefix > 0 && n_prefix < refine_below && depth + 1 <= steps - kMinSearchLevels) {
         if (in_dev) {
             h_in.resize((size_t)n_prefix * nn);
             if ((e = cudaMemcpyAsync(h_in.data(), prefix_buf, h_in.size(), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||

@@ -436,7 +436,8 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         cudaMemcpyAsync(mult.data(), d_mult, (size_t)k * 4, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         uint64_t part = 0, nd = 0;
-        int rc = dls::count_records(hg, hd, d_rec, k, counts.data(), &part, &nd, stream);
+        // canonic designs have large, uneven subtrees: always cut them to >= ~8 records per lane
+        int rc = dls::count_records(hg, hd, d_rec, k, counts.data(), &part, &nd, stream, 1200000);
         if (rc != DLS_OK) { cleanup(); return rc; }
         nodes += nd;
         for (long long i = 0; i < k; ++i) total += counts[(size_t)i] * (unsigned long long)mult[(size_t)i];
