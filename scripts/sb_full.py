@@ -31,17 +31,19 @@ def main():
     ap.add_argument("--parts", type=int, default=32)
     ap.add_argument("--budget-s", type=float, default=1e9)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--resume-from", default=None, help="extra JSONL file of finished parts (read only)")
     a = ap.parse_args()
     out = a.out or os.path.join(ROOT, "gpurun_out", "sb%d%s.jsonl" % (a.n, "vs" if a.vs else ""))
     d = D.default_split_depth(a.n, a.vs)
     total_wu = D.load().dls_split(a.n, int(a.vs), 1, d, None, 0)
     bounds = np.linspace(0, total_wu, a.parts + 1).astype(np.int64)
     done = {}
-    if os.path.exists(out):
-        for line in open(out):
-            r = json.loads(line)
-            if "part" in r and r.get("parts") == a.parts:
-                done[r["part"]] = r
+    for path in (a.resume_from, out):
+        if path and os.path.exists(path):
+            for line in open(path):
+                r = json.loads(line)
+                if "part" in r and r.get("parts") == a.parts:
+                    done[r["part"]] = r
     t_start = time.perf_counter()
     for k in range(a.parts):
         if k in done:
