@@ -262,7 +262,7 @@ def main():
             evs[i][1].record(stream)
             st = d_stats.cpu()
             counts.append(reduce_count(int(st[0])))
-            nodes_l.append(reduce_count(int(st[1]) + int(st[0])))
+            nodes_l.append(reduce_count(int(st[1])))
             assert int(st[2]) == 0
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall

@@ -126,8 +126,8 @@ int dls_count(int n, int symmetric, int fixed_first_row, int depth,
  *   d_prefixes     n_prefix prefix records.
  *   d_counts       n_prefix uint64 or NULL (zeroed by the call).
  *   d_stats        DLS_STATS_WORDS uint64 (zeroed by the call); after the stream
- *                  completes: [0] total count, [1] nodes above the leaves (nodes =
- *                  [1] + [0] when depth < n_steps), [2] prefix-error flag
+ *                  completes: [0] total count, [1] search nodes (every cell
+ *                  assignment below the records, complete squares included), [2] prefix-error flag
  *                  (nonzero = some record was inconsistent), [3] work-queue
  *                  cursor, [4] subtree donations, [5] busy lane-bursts,
  *                  [6] lane-bursts (lane utilisation = [5]/[6]), [7] subtrees

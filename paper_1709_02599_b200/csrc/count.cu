@@ -129,9 +129,7 @@ struct Masks;
 // N <= 8: row r is byte r&3 of R[r>>2], column c is byte c&3 of C[c>>2].
 // Tab: w0..w3 = multipliers of cell(t)'s row/col byte in R0,R1,C0,C1
 //      (1 << 8*(r&3) in the word holding the field, 0 in the other);
-//      w4, w5 = PRMT selectors (row, col byte index 0..7) of cell(t+1); bit 16 of
-//      w4 = "cell(t+1) is the last level" (leaf), bit 16 of w5 = not leaf (PRMT
-//      reads only bits 0..15 of its selector).
+//      w4, w5 = PRMT selectors (row, col byte index 0..7) of cell(t+1).
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t d;
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
@@ -164,10 +162,6 @@ struct Masks<N, VS, 0> {
         const uint32_t k = prmt(C0, C1, c.y);
         return G::ALLN & ~(r | k);                               // AllN ^ (Rows | Columns)
     }
-    __device__ __forceinline__ static void leaf_flags(const uint2 &c, int, int, uint32_t &leaf, uint32_t &notleaf) {
-        leaf = __umulhi(c.x, 65536u);
-        notleaf = __umulhi(c.y, 65536u);
-    }
 };
 
 // Word fields (e.g. vertical symmetry, N = 10): row r is field r % RPW32 of
@@ -175,8 +169,7 @@ struct Masks<N, VS, 0> {
 // straddles a word, so toggles are IMADs as in the byte layout, and a field is read
 // with one 64-bit funnel shift of the word pair.
 // Tab: w0..w3 = multipliers (1 << field offset, in the word holding the field);
-//      w4, w5 = bit offsets (0..63) of cell(t+1)'s row/col field in the pair;
-//      w6 = leaf, w7 = not leaf.
+//      w4, w5 = bit offsets (0..63) of cell(t+1)'s row/col field in the pair.
 template <int N, bool VS>
 struct Masks<N, VS, 1> {
     typedef Geo<N, VS> G;
@@ -204,10 +197,6 @@ struct Masks<N, VS, 1> {
         const uint32_t r = G::expand_row((uint32_t)((((u64)R1 << 32) | R0) >> c.x));
         const uint32_t k = (uint32_t)((((u64)C1 << 32) | C0) >> c.y);
         return G::ALLN & ~(r | k);
-    }
-    __device__ __forceinline__ static void leaf_flags(const uint4 &c, int, int, uint32_t &leaf, uint32_t &notleaf) {
-        leaf = c.z;
-        notleaf = c.w;
     }
 };
 
@@ -255,10 +244,7 @@ struct Masks<N, VS, 2> {
         const uint32_t k = field<G::WC>(C, c.z, c.w);
         return G::ALLN & ~(r | k);
     }
-    __device__ __forceinline__ static void leaf_flags(const uint4 &, int nl, int L, uint32_t &leaf, uint32_t &notleaf) {
-        leaf = nl == L ? 1u : 0u;
-        notleaf = 1u - leaf;
-    }
+
     typedef uint4 CT;
 };
 
@@ -333,8 +319,9 @@ template <int N, bool VS>
 struct Layout {
     static constexpr bool BYTES = Geo<N, VS>::BYTES;
     static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT != 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
-    static constexpr int CTW = BYTES ? 2 : 4;                 // words of a read entry
-    static constexpr int BLK_WORDS = 32 * (4 + CTW);          // words per transition block
+    // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
+    // so the toggle and read parts of a transition share one address register
+    static constexpr int BLK_WORDS = 32 * 8;                  // words per transition block
     // stack entries: N <= 16 bit candidate sets; u16 for the 64-bit layout (N = 9,
     // 10 DLS: long searches, so the smaller stack buys 1024 lanes per SM), else u32
     typedef typename std::conditional<Geo<N, VS>::LAYOUT == 2, uint16_t, uint32_t>::type SW;
@@ -359,8 +346,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         const Tab &e = p.tab[k >> 5];
         uint32_t *const blk = smem + (k >> 5) * LY::BLK_WORDS;
         reinterpret_cast<uint4 *>(blk)[k & 31] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
-        if (LY::BYTES) reinterpret_cast<uint2 *>(blk + 128)[k & 31] = make_uint2(e.w[4], e.w[5]);
-        else reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+        reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
@@ -369,11 +355,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
     __syncthreads();
     // slot of level l (l = -1 .. L): S[(l + 1) * NT]
     SW *const S = stack + tid;
-    // transition t: Fl[t * kBlk] (toggle part), Cl[t * kBlkC] (read part)
+    // transition t: Fl[t * kBlk] (toggle part), Cl at +512 bytes (read part)
     constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
-    constexpr int kBlkC = LY::BLK_WORDS / LY::CTW;           // block stride in CT units
+
     const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + LY::BLK_WORDS) + lane;
-    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128) + lane;
+    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128 + 4 * lane);
     const int kBlock = NT;
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte views for t-offsets
     const char *const Cb = reinterpret_cast<const char *>(Cl);
@@ -394,7 +380,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     int pid = -1;          // prefix being searched (n_prefix < 2^31)
     uint32_t cnt = 0;      // completions found for pid by this lane since the last flush
     // per-warp accumulators (shared memory, written by lane 0 / shared atomics):
-    // [0] squares, [1] nodes above the leaves, [2] donations, [3] busy lane-bursts,
+    // [0] squares, [1] nodes, [2] donations, [3] busy lane-bursts,
     // [4] lane-bursts -- keeps them out of the registers of the search loop
     // [5] (lane 0 only): ns between pool polls of this warp while idle
     __shared__ u64 wacc[32][6];
@@ -599,8 +585,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     cur = 0;
                 } else {
                     lvl = 1;                   // enter level 1: transition 0 reads cell(1)
-                    const uint32_t c = st.cand(Cl[0]);
-                    if (L == 1) { cnt = __popc(c); cur = 0; } else { cur = c; }
+                    cur = st.cand(Cl[0]);
                 }
             } else {                           // a donated subtree
                 for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * kBlock], 0u);
@@ -629,8 +614,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if (dn) sl[NT] = cur;                          // push L of level lvl
             if (mv) sl[0] = sibs;
             const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
-            const uint4 f = *reinterpret_cast<const uint4 *>(Fb + toff);
-            const CT cs = *reinterpret_cast<const CT *>(Cb + toff);
+            const char *const tp = Fb + toff;              // one address for both parts
+            const uint4 f = *reinterpret_cast<const uint4 *>(tp);
+            const CT cs = *reinterpret_cast<const CT *>(tp + 512);
             if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
                 st.toggle(f, dn ? b : sb, dn ? 0u : bb);                          // mark / unmark
             } else {
@@ -639,13 +625,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
             }
             const uint32_t c = st.cand(cs);               // AllN ^ (Rows | Columns) of cell(t+1)
             const bool adv = dn || mv;
-            const uint32_t c2 = adv ? c : 0u;
             const int nl = max(t + (adv ? 1 : 0), 0);
-            uint32_t leaf, notleaf;
-            M::leaf_flags(cs, nl, L, leaf, notleaf);
-            cnt32 += (uint32_t)__popc(c2) * leaf;          // complete squares at the last cell
+            // level L+1 is virtual: reaching it completes a square (P:93
+            // SquaresCnt++); its "cell" reads full row/column fields, so c = 0 there
+            cnt32 += nl > L ? 1u : 0u;
             ent32 += adv ? 1u : 0u;
-            cur = c2 * notleaf;
+            cur = adv ? c : 0u;
             lvl = nl;
         }
         cnt += cnt32;
@@ -665,7 +650,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         for (int w = 0; w < NT / 32; ++w)
             for (int k = 0; k < 5; ++k) a[k] += wacc[w][k];
         atomicAdd(p.stats + 0, a[0]);   // squares
-        atomicAdd(p.stats + 1, a[1]);   // nodes above the leaves
+        atomicAdd(p.stats + 1, a[1]);   // nodes (assignments, leaves included)
         atomicAdd(p.stats + 4, a[2]);   // donations
         atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
         atomicAdd(p.stats + 6, a[4]);   // lane-bursts
@@ -735,18 +720,17 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
                 e.w[3] = (uint32_t)(j / cpw);
             }
         }
-        if (t + 1 >= 1 && t + 1 <= L) {     // read part: cell(t+1)
-            const int i = cell_of(t + 1) / n, j = cell_of(t + 1) % n;
+        if (t + 1 >= 1 && L >= 1) {         // read part: cell(t+1); for t = L the virtual
+            // level L+1 reads cell L's row and column, which are full in a complete
+            // square, so its candidate set is empty
+            const int cl = std::min(t + 1, L);
+            const int i = cell_of(cl) / n, j = cell_of(cl) % n;
             if (bytes) {
-                const bool leaf = t + 1 == L;
-                e.w[4] = (uint32_t)i | (leaf ? 1u << 16 : 0u);
-                e.w[5] = (uint32_t)j | (leaf ? 0u : 1u << 16);
+                e.w[4] = (uint32_t)i;
+                e.w[5] = (uint32_t)j;
             } else if (lay == 1) {
-                const bool leaf = t + 1 == L;
                 e.w[4] = (uint32_t)(32 * (i / rpw32) + (i % rpw32) * rf);
                 e.w[5] = (uint32_t)(32 * (j / cpw32) + (j % cpw32) * cf);
-                e.w[6] = leaf ? 1u : 0u;
-                e.w[7] = leaf ? 0u : 1u;
             } else {
                 e.w[4] = (uint32_t)((i % rpw) * rf);
                 e.w[5] = (uint32_t)(i / rpw);
@@ -795,9 +779,8 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
 }
 
 size_t smem_bytes(int n, bool vs, int L, int nthreads) {
-    const size_t ct = layout_of(n, vs) == 0 ? 8 : 16;
     const size_t sw = layout_of(n, vs) == 2 ? 2 : 4;
-    return (size_t)(L + 2) * 32 * (16 + ct) + (size_t)(L + 2) * nthreads * sw;
+    return (size_t)(L + 2) * 32 * 32 + (size_t)(L + 2) * nthreads * sw;
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
@@ -1012,7 +995,7 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         return cuda_fail(e, "cudaMemcpyAsync(D2H)");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     if (out_total) *out_total = stats[0];
-    if (out_nodes) *out_nodes = stats[1] + (prm.L > 0 ? stats[0] : 0) + (u64)extra_nodes;
+    if (out_nodes) *out_nodes = stats[1] + (u64)extra_nodes;
     if (stats[2] || bad_prefix) {
         dls::set_error("dls_count: some prefix record is not a consistent depth-d prefix");
         return DLS_E_PREFIX;

@@ -52,9 +52,9 @@ def main():
         torch.cuda.synchronize()
         st = stats.cpu().tolist()
         ms = e0.elapsed_time(e1)
-        out.append({"launch": i, "ms": ms, "count": st[0], "nodes": st[1] + st[0], "err": st[2],
+        out.append({"launch": i, "ms": ms, "count": st[0], "nodes": st[1], "err": st[2],
                     "donations": st[4], "pool": st[7], "lane_util": st[5] / max(st[6], 1),
-                    "squares_per_s": st[0] / ms * 1e3, "nodes_per_s": (st[1] + st[0]) / ms * 1e3})
+                    "squares_per_s": st[0] / ms * 1e3, "nodes_per_s": st[1] / ms * 1e3})
     print(json.dumps({"n": a.n, "vs": a.vs, "depth": d, "n_prefix": int(recs.shape[0]),
                       "donate": os.environ.get("DLS_DONATE", "1"), "launches": out}), flush=True)
 
