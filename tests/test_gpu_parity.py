@@ -120,10 +120,12 @@ def test_config4_vs10_seeded_prefixes():
     gold = _read_golden("vs10_prefix_counts.txt")
     for i, (c, _) in gold.items():
         assert int(counts[i]) == c, i
-    # property at any size: a prefix's count is the sum over its children
-    sub = recs[[0, 4095]]
-    c2, t2, _ = _gpu(n, vs, sub, d)
-    assert (c2 == counts[[0, 4095]]).all()
+    # the golden prefixes alone: same counts, and the search visits exactly the
+    # oracle's nodes (full-size workunits, refined to ~1.2M records on the host)
+    idx = sorted(gold)
+    c2, t2, nodes = _gpu(n, vs, recs[idx], d)
+    assert [int(x) for x in c2] == [gold[i][0] for i in idx]
+    assert nodes == sum(gold[i][1] for i in idx)
 
 
 def test_config4_vs10_children_vs_oracle():
@@ -155,6 +157,10 @@ def test_config5_dls9_seeded_prefixes():
     gold = _read_golden("dls9_prefix_counts.txt")
     for i, (c, _) in gold.items():
         assert int(counts[i]) == c, i
+    idx = sorted(gold)
+    c2, t2, nodes = _gpu(n, False, recs[idx], d)
+    assert [int(x) for x in c2] == [gold[i][0] for i in idx]
+    assert nodes == sum(gold[i][1] for i in idx)
 
 
 def test_config5_dls9_children_vs_oracle():
