@@ -121,3 +121,53 @@ def test_count_refuses_without_gpu():
     with pytest.raises(D.DlsError) as e:
         D.dls_count(6, 8, pre)
     assert e.value.code == B.DLS_E_NODEVICE
+
+
+@pytest.mark.parametrize("n,vs,extra", [(6, False, 3), (7, False, 4), (8, True, 3), (10, True, 2)])
+def test_refine_equals_oracle_children(n, vs, extra):
+    """dls_refine (P:481 below given records) == the oracle's enumeration of the
+    next `extra` plan cells below each record, in record order."""
+    d = D.default_split_depth(n, vs)
+    if n == 10:
+        recs = synth.diagonal_prefixes(3, n, 3, vs=True)
+    else:
+        recs = D.dls_split(n, d, vs)[:5]
+    kids, parent = D.dls_refine(n, d, recs, d + extra, vs)
+    order = oracle.plan(n, vs)
+    want, want_par = [], []
+    for p, r in enumerate(recs):
+        k = oracle.prefixes(n, vs, synth.to_int_grid(r), order[d:], extra)
+        want.extend(k)
+        want_par.extend([p] * len(k))
+    assert len(kids) == len(want)
+    assert (synth.to_int_grid(kids) == np.array(want)).all()
+    assert parent.tolist() == want_par
+
+
+def test_refine_rejects_bad_records():
+    n = 7
+    d = D.default_split_depth(n)
+    recs = D.dls_split(n, d)[:3].copy()
+    recs[1, 2, 2] = recs[1, 1, 1]          # repeated value on the main diagonal
+    with pytest.raises(D.DlsError) as e:
+        D.dls_refine(n, d, recs, d + 2)
+    assert e.value.code == B.DLS_E_PREFIX
+    with pytest.raises(D.DlsError):
+        D.dls_refine(n, d, recs[:1], d - 1)
+
+
+def test_reference_arm_json():
+    import json
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DLS_REF_STEP_SECONDS="0.5")
+    out = subprocess.run([sys.executable, ROOT + "/bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "cpu_baseline", "e2e", "config"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
