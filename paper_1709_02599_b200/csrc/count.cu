@@ -944,6 +944,9 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         depth_run = d1;
     }
     const bool refined = depth_run != depth;
+    if (getenv("DLS_TIMING"))   // count_records timing
+        fprintf(stderr, "[count_records] %lld records at depth %d -> %lld at depth %d\n", (long long)n_prefix, depth,
+                (long long)n_rec, depth_run);
 
     const bool counts_host = out_counts && n_prefix > 0 && !is_device_ptr(out_counts);
     const bool stage_records = n_rec > 0 && (refined || !in_dev);

@@ -31,6 +31,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -41,6 +44,21 @@
 namespace {
 
 typedef unsigned long long u64;
+
+// DLS_TIMING=1: phase times of the symmetry-broken driver on stderr
+struct PhaseTimer {
+    bool on = getenv("DLS_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what, cudaStream_t s) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[dls_count_sb] %-28s %9.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 constexpr int kMaxGroup = 1536;        // 2 * 2^5 * 4! for N = 10
 constexpr int kSbThreads = 256;
 
@@ -361,6 +379,7 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         return DLS_E_ARG;
     }
     cudaStream_t s = (cudaStream_t)stream;
+    PhaseTimer timer;
     const int nn = n * n;
     const int dd = base.diag_depth;
     // the hourglass plan lists the diagonal cells exactly as the standard plan
@@ -385,6 +404,7 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
     }
     std::vector<uint8_t> all((size_t)std::max<int64_t>(n_all, 1) * nn);
     dls_split(n, symmetric, 1, dd, all.data(), n_all);
+    timer.mark("host split (diagonals)", s);
     const int64_t n_diag = diag_end - diag_begin;
     const uint8_t *const diag_base = all.data() + diag_begin * nn;
     const int64_t chunk = 1 << 20;
@@ -425,6 +445,7 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         unsigned long long cnt[4];
         cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s);
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cleanup(); return fail(e, "hourglass_kernel"); }
+        timer.mark("H2D + hourglass kernel", s);
         if (cnt[2]) { cleanup(); dls::set_error("dls_count_sb: canonic buffer overflow"); return DLS_E_ARG; }
         hourglasses += cnt[0];
         classes += cnt[1];
@@ -441,6 +462,7 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         if (rc != DLS_OK) { cleanup(); return rc; }
         nodes += nd;
         for (long long i = 0; i < k; ++i) total += counts[(size_t)i] * (unsigned long long)mult[(size_t)i];
+        timer.mark("refine + search canonic", s);
     }
     cleanup();
     if (out_total) *out_total = total;
