@@ -12,8 +12,12 @@
 // dls::refine   : from given depth-d0 records, cells [d0, d1), with parent index
 //                 (used by dls_count to cut few large workunits into many)
 // dls::valid_record : host check of one record against a depth-d pattern
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -135,10 +139,10 @@ class Enumerator {
 
 }  // namespace
 
-namespace dls {
+namespace {
 
-int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in, uint8_t *out,
-               uint32_t *parent, int64_t capacity, int64_t *extra_nodes) {
+int64_t refine_serial(const dls::Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in, uint8_t *out,
+                      uint32_t *parent, int64_t capacity, int64_t *extra_nodes) {
     const int nn = plan.n * plan.n;
     Enumerator en(plan, d0, d1);
     std::vector<int64_t> lv(d1 - d0 + 1, 0);
@@ -161,6 +165,81 @@ int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in
         int64_t s = 0;
         for (int k = 0; k < d1 - d0; ++k) s += lv[k];
         *extra_nodes = s;
+    }
+    return total;
+}
+
+int host_threads() {
+    if (const char *e = getenv("DLS_HOST_THREADS")) return std::max(1, atoi(e));
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::min(32u, std::max(1u, hc));
+}
+
+}  // namespace
+
+namespace dls {
+
+// Multi-threaded: contiguous chunks of the input records are enumerated by
+// different threads (a counting pass, then a filling pass at the chunk offsets),
+// so the output order is exactly the serial one.  With too few input records the
+// first level is expanded serially to make enough roots.
+int64_t refine(const Plan &plan, int d0, int d1, const uint8_t *in, int64_t n_in, uint8_t *out,
+               uint32_t *parent, int64_t capacity, int64_t *extra_nodes) {
+    const int T = host_threads();
+    const int nn = plan.n * plan.n;
+    if (T <= 1 || d1 - d0 < 2 || n_in == 0)
+        return refine_serial(plan, d0, d1, in, n_in, out, parent, capacity, extra_nodes);
+    if (n_in < 16 * T) {
+        // expand one level to get more roots (their parents map back to `in`)
+        const int64_t r = refine_serial(plan, d0, d0 + 1, in, n_in, nullptr, nullptr, 0, nullptr);
+        std::vector<uint8_t> roots((size_t)std::max<int64_t>(r, 1) * nn);
+        std::vector<uint32_t> rpar((size_t)std::max<int64_t>(r, 1));
+        refine_serial(plan, d0, d0 + 1, in, n_in, roots.data(), rpar.data(), r, nullptr);
+        std::vector<uint32_t> par2;
+        if (parent && capacity > 0) par2.resize((size_t)capacity);
+        int64_t extra2 = 0;
+        const int64_t total = refine(plan, d0 + 1, d1, roots.data(), r, out, parent ? par2.data() : nullptr,
+                                     capacity, extra_nodes ? &extra2 : nullptr);
+        if (parent)
+            for (int64_t i = 0; i < std::min(total, capacity); ++i) parent[i] = rpar[par2[(size_t)i]];
+        if (extra_nodes) *extra_nodes = r + extra2;
+        return total;
+    }
+    const int chunks = (int)std::min<int64_t>(n_in, 4 * T);
+    std::vector<int64_t> lo(chunks + 1), cnt(chunks, 0), ext(chunks, 0);
+    for (int c = 0; c <= chunks; ++c) lo[c] = n_in * c / chunks;
+    auto run = [&](bool fill, const std::vector<int64_t> &off) {
+        std::vector<std::thread> th;
+        std::atomic<int> next(0);
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&]() {
+                for (int c = next++; c < chunks; c = next++) {
+                    if (!fill) {
+                        cnt[c] = refine_serial(plan, d0, d1, in + lo[c] * nn, lo[c + 1] - lo[c], nullptr, nullptr, 0,
+                                               &ext[c]);
+                    } else {
+                        const int64_t o = off[c];
+                        const int64_t room = std::max<int64_t>(0, std::min(cnt[c], capacity - o));
+                        if (room <= 0) continue;
+                        uint32_t *pp = parent ? parent + o : nullptr;
+                        refine_serial(plan, d0, d1, in + lo[c] * nn, lo[c + 1] - lo[c], out + o * nn, pp, room,
+                                      nullptr);
+                        if (pp)
+                            for (int64_t i = 0; i < room; ++i) pp[i] += (uint32_t)lo[c];
+                    }
+                }
+            });
+        for (auto &x : th) x.join();
+    };
+    run(false, {});
+    std::vector<int64_t> off(chunks + 1, 0);
+    for (int c = 0; c < chunks; ++c) off[c + 1] = off[c] + cnt[c];
+    const int64_t total = off[chunks];
+    if (out && capacity > 0) run(true, off);
+    if (extra_nodes) {
+        int64_t e = 0;
+        for (int c = 0; c < chunks; ++c) e += ext[c];
+        *extra_nodes = e;
     }
     return total;
 }
