@@ -88,6 +88,19 @@ int64_t dls_split(int n, int symmetric, int fixed_first_row, int depth,
                   uint8_t *out_prefixes, int64_t capacity);
 
 /*
+ * dls_emit -- the optional compact emit of squares (small n): the same search as
+ * dls_count_async, but every completed square is written as an n*n record
+ * (row-major values) into d_out, in no particular order.
+ *   d_prefixes     device, n_prefix depth-`depth` records;
+ *   d_out          device, capacity*n*n bytes (capacity may be 0: count only).
+ * Synchronous.  Returns the number of completions (records written: min(that,
+ * capacity)), or a DLS_E_* code.
+ */
+int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth,
+                 const uint8_t *d_prefixes, int64_t n_prefix,
+                 uint8_t *d_out, int64_t capacity, void *stream);
+
+/*
  * dls_refine -- the same decomposition applied below given records: every
  * consistent assignment of plan cells [depth, depth2) below each of the n_in
  * depth-`depth` records `in` (host), in record order then depth-first order.

@@ -19,7 +19,7 @@ DLS_MAX_ORDER = 10
 DLS_STATS_WORDS = 8
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
-EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_count",
+EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
            "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_kernel_launches")
 
 _lib = None
@@ -55,6 +55,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_split.restype = c_i64
     lib.dls_refine.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, c_int, vp, vp, c_i64]
     lib.dls_refine.restype = c_i64
+    lib.dls_emit.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, c_i64, vp]
+    lib.dls_emit.restype = c_i64
     lib.dls_count.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp, vp]
     lib.dls_count.restype = c_int
     lib.dls_count_async.argtypes = [c_int, c_int, c_int, c_int, vp, c_i64, vp, vp, vp]
@@ -188,6 +190,19 @@ def dls_count_sb_range(n: int, begin: int, end: int, symmetric: bool = False, st
     rc = load().dls_count_sb_range(n, int(symmetric), begin, end, *[ctypes.addressof(v) for v in vals], stream or None)
     _check(rc, "dls_count_sb_range")
     return {"count": vals[0].value, "hourglasses": vals[1].value, "classes": vals[2].value, "nodes": vals[3].value}
+
+
+def dls_emit(n: int, depth: int, d_prefixes, d_out, symmetric: bool = False, fixed_first_row: bool = True,
+             stream: Optional[int] = None) -> int:
+    """Write every completion of the (CUDA) records into d_out (CUDA uint8, (cap, n, n));
+    returns the number of completions."""
+    pp, k1 = _ptr(d_prefixes)
+    op, k2 = _ptr(d_out)
+    cap = int(d_out.shape[0]) if d_out is not None else 0
+    got = load().dls_emit(n, int(symmetric), int(fixed_first_row), depth, pp or None, int(d_prefixes.shape[0]),
+                          op or None, cap, stream or None)
+    _check(got, "dls_emit")
+    return int(got)
 
 
 def dls_kernel_launches() -> int:

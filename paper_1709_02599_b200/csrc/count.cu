@@ -81,6 +81,9 @@ struct Params {
     int donate;              // enable warp-level subtree donation
     int min_donate;          // smallest donated subtree (levels below the split)
     uint32_t total_warps;    // warps of the grid (exit once all registered)
+    uint8_t *emit;           // emit kernels: complete squares, n*n bytes each
+    long long emit_cap;      //               capacity (records)
+    uint8_t level_cell[kMaxLevels + 2];   // cell (i*n+j) of level l = 1..L
     Tab tab[kMaxLevels + 2]; // tab[t + 1], t = -1 .. L
 };
 
@@ -327,7 +330,27 @@ struct Layout {
     typedef typename std::conditional<Geo<N, VS>::LAYOUT == 2, uint16_t, uint32_t>::type SW;
 };
 
-template <int N, bool VS>
+// Rebuild a complete square from the workunit record and the lane's stack and
+// append it to p.emit (the optional compact emit of squares for small N).
+template <int N, bool VS, class SW>
+__device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, int NT) {
+    typedef Geo<N, VS> G;
+    const u64 slot = atomicAdd(p.stats + 7, 1ull);
+    if ((long long)slot >= p.emit_cap) return;
+    uint8_t *dst = p.emit + slot * (u64)(N * N);
+    const uint8_t *rec = p.prefixes + (u64)pid * (u64)(N * N);
+    for (int c = 0; c < N * N; ++c) dst[c] = rec[c];
+    for (int l = 1; l <= p.L; ++l) {
+        const int cell = p.level_cell[l];
+        const int pos = __ffs((uint32_t)S[(l + 1) * NT]) - 1;
+        // internal bit position -> value (VS: positions >= N/2 hold N-1-(p-N/2))
+        const int v = (!VS || pos < G::H) ? pos : N - 1 - (pos - G::H);
+        dst[cell] = (uint8_t)v;
+        if (VS) dst[(cell / N) * N + (N - 1 - cell % N)] = (uint8_t)(N - 1 - v);
+    }
+}
+
+template <int N, bool VS, bool EMIT>
 __global__ void __launch_bounds__(1024, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
@@ -629,6 +652,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             // level L+1 is virtual: reaching it completes a square (P:93
             // SquaresCnt++); its "cell" reads full row/column fields, so c = 0 there
             cnt32 += nl > L ? 1u : 0u;
+            if (EMIT && nl > L) emit_square<N, VS, SW>(p, pid, S, NT);
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
             lvl = nl;
@@ -654,27 +678,27 @@ dls_search_kernel(const __grid_constant__ Params p) {
         atomicAdd(p.stats + 4, a[2]);   // donations
         atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
         atomicAdd(p.stats + 6, a[4]);   // lane-bursts
-        atomicMax(p.stats + 7, (u64)ld_acquire(pool + 3));   // subtrees published to the pool
+        if (!EMIT) atomicMax(p.stats + 7, (u64)ld_acquire(pool + 3));   // subtrees published to the pool
     }
 }
 
 typedef void (*KernelFn)(Params);
 
 template <int N, bool VS>
-KernelFn kernel_for() { return dls_search_kernel<N, VS>; }
+KernelFn kernel_for(bool emit) { return emit ? dls_search_kernel<N, VS, true> : dls_search_kernel<N, VS, false>; }
 
-KernelFn pick_kernel(int n, bool vs) {
+KernelFn pick_kernel(int n, bool vs, bool emit) {
     switch (n) {
-        case 1: return kernel_for<1, false>();
-        case 2: return vs ? kernel_for<2, true>() : kernel_for<2, false>();
-        case 3: return kernel_for<3, false>();
-        case 4: return vs ? kernel_for<4, true>() : kernel_for<4, false>();
-        case 5: return kernel_for<5, false>();
-        case 6: return vs ? kernel_for<6, true>() : kernel_for<6, false>();
-        case 7: return kernel_for<7, false>();
-        case 8: return vs ? kernel_for<8, true>() : kernel_for<8, false>();
-        case 9: return kernel_for<9, false>();
-        case 10: return vs ? kernel_for<10, true>() : kernel_for<10, false>();
+        case 1: return kernel_for<1, false>(emit);
+        case 2: return vs ? kernel_for<2, true>(emit) : kernel_for<2, false>(emit);
+        case 3: return kernel_for<3, false>(emit);
+        case 4: return vs ? kernel_for<4, true>(emit) : kernel_for<4, false>(emit);
+        case 5: return kernel_for<5, false>(emit);
+        case 6: return vs ? kernel_for<6, true>(emit) : kernel_for<6, false>(emit);
+        case 7: return kernel_for<7, false>(emit);
+        case 8: return vs ? kernel_for<8, true>(emit) : kernel_for<8, false>(emit);
+        case 9: return kernel_for<9, false>(emit);
+        case 10: return vs ? kernel_for<10, true>(emit) : kernel_for<10, false>(emit);
         default: return nullptr;
     }
 }
@@ -754,6 +778,7 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     prm->L = steps - depth;
     std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.end());
     fill_tab(n, symmetric, level_cells, prm->tab);
+    for (size_t l = 0; l < level_cells.size(); ++l) prm->level_cell[l + 1] = (uint8_t)level_cells[l];
     // assigned-cell pattern of a depth-`depth` prefix
     auto set = [&](int c) { prm->pat[c >> 6] |= 1ull << (c & 63); };
     for (int c = 0; c < n * n; ++c)
@@ -784,7 +809,7 @@ size_t smem_bytes(int n, bool vs, int L, int nthreads) {
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
-    KernelFn fn = pick_kernel(n, vs);
+    KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
     cudaError_t e;
     int dev = 0, sms = 0, smem_max = 0;
@@ -1017,4 +1042,37 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
         return DLS_E_ARG;
     }
     return dls::count_records(plan, depth, prefix_buf, n_prefix, out_counts, out_total, out_nodes, stream);
+}
+
+extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth, const uint8_t *d_prefixes,
+                            int64_t n_prefix, uint8_t *d_out, int64_t capacity, void *stream) {
+    int rc = have_device();
+    if (rc) return rc;
+    if (n_prefix < 0 || n_prefix >= (int64_t)1 << 31 || (n_prefix > 0 && !d_prefixes) || capacity < 0 ||
+        (capacity > 0 && !d_out) || !is_device_ptr(d_prefixes) || (capacity > 0 && !is_device_ptr(d_out))) {
+        dls::set_error("dls_emit: bad pointers / sizes (device buffers required)");
+        return DLS_E_ARG;
+    }
+    Params prm;
+    if ((rc = prepare(n, symmetric, fixed_first_row, depth, &prm))) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    u64 *d_stats = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&d_stats, DLS_STATS_WORDS * sizeof(u64), s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    cudaMemsetAsync(d_stats, 0, DLS_STATS_WORDS * sizeof(u64), s);
+    prm.prefixes = d_prefixes;
+    prm.n_prefix = n_prefix;
+    prm.stats = d_stats;
+    prm.emit = d_out ? d_out : (uint8_t *)d_stats;   // non-null selects the emit kernel
+    prm.emit_cap = capacity;
+    if (n_prefix > 0 && (rc = launch(n, symmetric, prm, s))) { cudaFreeAsync(d_stats, s); return rc; }
+    u64 stats[DLS_STATS_WORDS];
+    cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d_stats, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "dls_emit");
+    if (stats[2]) {
+        dls::set_error("dls_emit: some prefix record is not a consistent depth-d prefix");
+        return DLS_E_PREFIX;
+    }
+    return (int64_t)stats[0];
 }

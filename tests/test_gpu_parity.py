@@ -289,3 +289,24 @@ def test_few_workunits_spread_by_device_pool(n, vs, k):
     assert (out.cpu().numpy().astype(np.uint64) == want).all()
     st = stats.cpu().tolist()
     assert st[2] == 0 and st[0] == int(want.sum()) and st[1] == want_nodes
+
+
+@pytest.mark.parametrize("n,vs,fixed", [(4, False, True), (5, False, True), (6, False, True), (5, False, False),
+                                        (4, True, True), (6, True, True), (6, True, False)])
+def test_emit_squares_equal_oracle(n, vs, fixed):
+    """The compact emit of squares (north_star (4)): the very same squares as the oracle."""
+    import torch
+    d = D.default_split_depth(n, vs, fixed)
+    recs = torch.from_numpy(D.dls_split(n, d, vs, fixed)).cuda()
+    want = oracle.squares(n, vs, oracle.first_row_grid(n) if fixed else oracle.empty_grid(n))
+    total = D.dls_emit(n, d, recs, None, vs, fixed)                      # count only
+    assert total == len(want)
+    out = torch.zeros((total + 5, n, n), dtype=torch.uint8, device="cuda")
+    assert D.dls_emit(n, d, recs, out, vs, fixed) == total
+    got = out[:total].cpu().numpy().astype(np.int64)
+    key = lambda a: sorted(tuple(x.reshape(-1).tolist()) for x in a)
+    assert key(got) == key(want)
+    for sq in got:
+        assert oracle.is_diagonal(sq) and (not vs or oracle.is_vertically_symmetric(sq))
+    small = torch.zeros((3, n, n), dtype=torch.uint8, device="cuda")
+    assert D.dls_emit(n, d, recs, small, vs, fixed) == total               # capacity < total
