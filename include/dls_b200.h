@@ -190,6 +190,19 @@ int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int64_t diag_en
                        uint64_t *out_nodes, void *stream);
 
 /*
+ * dls_count_cells -- number of consistent assignments of the listed cells below
+ * one partial square: e.g. the first k row-major cells of an order-n DLS with row
+ * 0 fixed, N_n^k of the Monte Carlo section.  The listed diagonal cells
+ * are enumerated on the host, the rest by the GPU search (virtual last level).
+ *   record         host, n*n: the given cells (row 0 must be complete), 0xFF elsewhere;
+ *   cells          host, n_cells distinct empty cells (i*n+j; left half if symmetric).
+ *   out_total / out_nodes   host.
+ * Synchronous.  Returns DLS_OK or a DLS_E_* code.
+ */
+int dls_count_cells(int n, int symmetric, const uint8_t *record, const int32_t *cells,
+                    int n_cells, uint64_t *out_total, uint64_t *out_nodes, void *stream);
+
+/*
  * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
  * per call (for the bench's launch count): the search kernel only.
  */

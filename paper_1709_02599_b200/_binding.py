@@ -20,7 +20,8 @@ DLS_STATS_WORDS = 8
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
-           "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_kernel_launches")
+           "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_count_cells",
+           "dls_kernel_launches")
 
 _lib = None
 
@@ -67,6 +68,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_count_sb.restype = c_int
     lib.dls_count_sb_range.argtypes = [c_int, c_int, c_i64, c_i64, vp, vp, vp, vp, vp]
     lib.dls_count_sb_range.restype = c_int
+    lib.dls_count_cells.argtypes = [c_int, c_int, vp, vp, c_int, vp, vp, vp]
+    lib.dls_count_cells.restype = c_int
     lib.dls_kernel_launches.restype = c_int
     _lib = lib
     return lib
@@ -203,6 +206,18 @@ def dls_emit(n: int, depth: int, d_prefixes, d_out, symmetric: bool = False, fix
                           op or None, cap, stream or None)
     _check(got, "dls_emit")
     return int(got)
+
+
+def dls_count_cells(n: int, record: np.ndarray, cells, symmetric: bool = False, stream: Optional[int] = None):
+    """Consistent assignments of `cells` below `record` -> (count, nodes)."""
+    rec = np.ascontiguousarray(record, dtype=np.uint8).reshape(-1)
+    cl = np.ascontiguousarray(np.asarray(list(cells), dtype=np.int32))
+    tot = ctypes.c_uint64(0)
+    nodes = ctypes.c_uint64(0)
+    rc = load().dls_count_cells(n, int(symmetric), rec.ctypes.data, cl.ctypes.data if len(cl) else None, len(cl),
+                                ctypes.addressof(tot), ctypes.addressof(nodes), stream or None)
+    _check(rc, "dls_count_cells")
+    return int(tot.value), int(nodes.value)
 
 
 def dls_kernel_launches() -> int:

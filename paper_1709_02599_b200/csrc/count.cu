@@ -745,10 +745,10 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             }
         }
         if (t + 1 >= 1 && L >= 1) {         // read part: cell(t+1); for t = L the virtual
-            // level L+1 reads cell L's row and column, which are full in a complete
-            // square, so its candidate set is empty
+            // level L+1 reads row 0 (assigned in every record, hence full), so its
+            // candidate set is empty
             const int cl = std::min(t + 1, L);
-            const int i = cell_of(cl) / n, j = cell_of(cl) % n;
+            const int i = t + 1 > L ? 0 : cell_of(cl) / n, j = cell_of(cl) % n;
             if (bytes) {
                 e.w[4] = (uint32_t)i;
                 e.w[5] = (uint32_t)j;
@@ -770,6 +770,12 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     const int n = plan.n;
     const bool symmetric = plan.vs;
     const int steps = (int)plan.cells.size();
+    for (int j = 0; j < n; ++j)
+        if (!plan.pre[j] && std::find(plan.cells.begin(), plan.cells.begin() + std::min(depth, steps), j) ==
+                                plan.cells.begin() + std::min(depth, steps)) {
+            dls::set_error("dls_count: row 0 must be assigned in the records");
+            return DLS_E_ARG;
+        }
     if (depth < plan.diag_depth || depth > steps) {
         dls::set_error("dls_count: depth must satisfy diag_depth <= depth <= n_steps");
         return DLS_E_ARG;
@@ -1075,4 +1081,59 @@ extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth
         return DLS_E_PREFIX;
     }
     return (int64_t)stats[0];
+}
+
+extern "C" int dls_count_cells(int n, int symmetric, const uint8_t *record, const int32_t *cells, int n_cells,
+                               uint64_t *out_total, uint64_t *out_nodes, void *stream) {
+    if (n < 1 || n > DLS_MAX_ORDER || (symmetric && n % 2) || !record || n_cells < 0 || (n_cells && !cells)) {
+        dls::set_error("dls_count_cells: bad arguments");
+        return DLS_E_ARG;
+    }
+    const int nn = n * n;
+    uint8_t pre[DLS_MAX_ORDER * DLS_MAX_ORDER] = {};
+    for (int c = 0; c < nn; ++c) pre[c] = record[c] != DLS_EMPTY;
+    for (int j = 0; j < n; ++j)
+        if (!pre[j]) { dls::set_error("dls_count_cells: row 0 of the record must be assigned"); return DLS_E_ARG; }
+    // the listed diagonal cells first (the GPU search tracks rows and columns only)
+    std::vector<int> head, rest;
+    std::vector<uint8_t> seen(nn, 0);
+    for (int k = 0; k < n_cells; ++k) {
+        const int c = cells[k];
+        if (c < 0 || c >= nn || pre[c] || seen[c] || (symmetric && 2 * (c % n) > n - 1)) {
+            dls::set_error("dls_count_cells: cells must be distinct, empty in the record (left half if symmetric)");
+            return DLS_E_ARG;
+        }
+        seen[c] = 1;
+        const int i = c / n, j = c % n;
+        const bool diag = i == j || i + j == n - 1 || (symmetric && (i == n - 1 - j || i + (n - 1 - j) == n - 1));
+        (diag ? head : rest).push_back(c);
+    }
+    const int dd = (int)head.size();
+    head.insert(head.end(), rest.begin(), rest.end());
+    dls::Plan plan;
+    if (!dls::make_plan_from(n, symmetric, pre, head, &plan)) {
+        dls::set_error("dls_count_cells: unsupported order");
+        return DLS_E_ARG;
+    }
+    plan.cells.resize(n_cells);
+    plan.forced.resize(n_cells);
+    plan.diag_depth = dd;
+    // records at the diagonal depth (host), then the GPU search of the other cells
+    const int64_t k = dls::refine(plan, 0, dd, record, 1, nullptr, nullptr, 0, nullptr);
+    if (k < 0) return (int)k;
+    std::vector<uint8_t> recs((size_t)std::max<int64_t>(k, 1) * nn);
+    int64_t extra = 0;
+    dls::refine(plan, 0, dd, record, 1, recs.data(), nullptr, k, &extra);
+    uint64_t total = 0, nodes = 0;
+    if (k > 0) {
+        if (dd == n_cells) {
+            total = (uint64_t)k;
+        } else {
+            const int rc = dls::count_records(plan, dd, recs.data(), k, nullptr, &total, &nodes, stream);
+            if (rc) return rc;
+        }
+    }
+    if (out_total) *out_total = total;
+    if (out_nodes) *out_nodes = nodes + (uint64_t)extra;
+    return DLS_OK;
 }

@@ -310,3 +310,22 @@ def test_emit_squares_equal_oracle(n, vs, fixed):
         assert oracle.is_diagonal(sq) and (not vs or oracle.is_vertically_symmetric(sq))
     small = torch.zeros((3, n, n), dtype=torch.uint8, device="cuda")
     assert D.dls_emit(n, d, recs, small, vs, fixed) == total               # capacity < total
+
+
+@pytest.mark.parametrize("n,vs,k", [(7, False, 21), (8, False, 26), (8, True, 24), (6, False, 20)])
+def test_count_cells_row_major_vs_oracle(n, vs, k):
+    """N_n^k: consistent assignments of the first k row-major cells, row 0 fixed."""
+    g = oracle.first_row_grid(n)
+    cells = [c for c in range(n, k) if not vs or 2 * (c % n) <= n - 1]
+    want = oracle.count_prefixes(n, vs, g, cells, len(cells))
+    got, _ = D.dls_count_cells(n, np.where(g < 0, 255, g).astype(np.uint8), cells, vs)
+    assert got == want
+
+
+@pytest.mark.parametrize("k,key", [(30, "dls10_k30_prefixes"), (32, "dls10_k32_prefixes")])
+def test_count_cells_dls10_paper(k, key):
+    """N_10^30 = 284 086 571 712 and N_10^32 = 12 611 543 636 160."""
+    n = 10
+    g = oracle.first_row_grid(n)
+    got, _ = D.dls_count_cells(n, np.where(g < 0, 255, g).astype(np.uint8), list(range(n, k)))
+    assert got == paper_counts()[key]
