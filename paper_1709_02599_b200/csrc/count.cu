@@ -770,12 +770,16 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     const int n = plan.n;
     const bool symmetric = plan.vs;
     const int steps = (int)plan.cells.size();
-    for (int j = 0; j < n; ++j)
-        if (!plan.pre[j] && std::find(plan.cells.begin(), plan.cells.begin() + std::min(depth, steps), j) ==
-                                plan.cells.begin() + std::min(depth, steps)) {
-            dls::set_error("dls_count: row 0 must be assigned in the records");
-            return DLS_E_ARG;
+    {   // the virtual last level reads row 0: it must be assigned in every record
+        const auto first = plan.cells.begin(), last = plan.cells.begin() + std::min(depth, steps);
+        for (int j = 0; j < n; ++j) {
+            const int jm = symmetric ? n - 1 - j : j;   // VS plans list left-half cells only
+            if (!plan.pre[j] && std::find(first, last, j) == last && std::find(first, last, jm) == last) {
+                dls::set_error("dls_count: row 0 must be assigned in the records");
+                return DLS_E_ARG;
+            }
         }
+    }
     if (depth < plan.diag_depth || depth > steps) {
         dls::set_error("dls_count: depth must satisfy diag_depth <= depth <= n_steps");
         return DLS_E_ARG;
