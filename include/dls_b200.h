@@ -203,6 +203,18 @@ int dls_count_cells(int n, int symmetric, const uint8_t *record, const int32_t *
                     int n_cells, uint64_t *out_total, uint64_t *out_nodes, void *stream);
 
 /*
+ * dls_random_prefix -- one random descent of the Monte Carlo estimate of Section
+ * 5.3: the listed empty cells of `record` are assigned in order, each
+ * uniformly among its consistent values (splitmix64 stream of `seed`), into
+ * out_record (host, n*n); *out_weight = product of the numbers of consistent values
+ * (0 if some cell had none).  mean(weight x completions(out_record)) over
+ * independent seeds is an unbiased estimate of the completions of `record`.
+ * Host only.  Returns DLS_OK, DLS_E_ARG or DLS_E_PREFIX.
+ */
+int dls_random_prefix(int n, int symmetric, const uint8_t *record, const int32_t *cells,
+                      int n_cells, uint64_t seed, uint8_t *out_record, double *out_weight);
+
+/*
  * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
  * per call (for the bench's launch count): the search kernel only.
  */

@@ -6,7 +6,7 @@ P:235-258) on every lane of a persistent CUDA kernel.  The C ABI is
 include/dls_b200.h; this package is its thin binding plus convenience wrappers.
 """
 from ._binding import (DLS_EMPTY, DLS_MAX_ORDER, DLS_STATS_WORDS, DlsError, dls_canonize, dls_count,  # noqa: F401
-                       dls_count_async, dls_count_cells, dls_count_sb, dls_count_sb_range, dls_emit,
+                       dls_count_async, dls_count_cells, dls_count_sb, dls_count_sb_range, dls_emit, dls_random_prefix,
                        dls_kernel_launches, dls_plan, dls_refine, dls_split,
                        dls_version,
                        lib_path, load)

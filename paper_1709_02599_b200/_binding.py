@@ -21,7 +21,7 @@ DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
            "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_count_cells",
-           "dls_kernel_launches")
+           "dls_random_prefix", "dls_kernel_launches")
 
 _lib = None
 
@@ -70,6 +70,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_count_sb_range.restype = c_int
     lib.dls_count_cells.argtypes = [c_int, c_int, vp, vp, c_int, vp, vp, vp]
     lib.dls_count_cells.restype = c_int
+    lib.dls_random_prefix.argtypes = [c_int, c_int, vp, vp, c_int, ctypes.c_uint64, vp, vp]
+    lib.dls_random_prefix.restype = c_int
     lib.dls_kernel_launches.restype = c_int
     _lib = lib
     return lib
@@ -218,6 +220,18 @@ def dls_count_cells(n: int, record: np.ndarray, cells, symmetric: bool = False, 
                                 ctypes.addressof(tot), ctypes.addressof(nodes), stream or None)
     _check(rc, "dls_count_cells")
     return int(tot.value), int(nodes.value)
+
+
+def dls_random_prefix(n: int, record: np.ndarray, cells, seed: int, symmetric: bool = False):
+    """One Knuth random descent -> (record (n, n) uint8, weight)."""
+    rec = np.ascontiguousarray(record, dtype=np.uint8).reshape(-1)
+    cl = np.ascontiguousarray(np.asarray(list(cells), dtype=np.int32))
+    out = np.empty(n * n, dtype=np.uint8)
+    w = ctypes.c_double(0.0)
+    rc = load().dls_random_prefix(n, int(symmetric), rec.ctypes.data, cl.ctypes.data if len(cl) else None, len(cl),
+                                  ctypes.c_uint64(seed & (2 ** 64 - 1)), out.ctypes.data, ctypes.addressof(w))
+    _check(rc, "dls_random_prefix")
+    return out.reshape(n, n), float(w.value)
 
 
 def dls_kernel_launches() -> int:

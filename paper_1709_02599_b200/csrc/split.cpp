@@ -304,3 +304,84 @@ extern "C" int64_t dls_refine(int n, int symmetric, int fixed_first_row, int dep
         }
     return dls::refine(plan, depth, depth2, in, n_in, out, parent, capacity, nullptr);
 }
+
+// Random descent for the Monte Carlo estimate of Section 5.3: the
+// cells are assigned in the given order, each uniformly among its consistent
+// values (counter-based splitmix64 stream of `seed`); *out_weight = product of
+// the numbers of consistent values met (0 at a dead end).  E[weight x completions]
+// over the descent = number of completions of `record` (Knuth's estimator).
+extern "C" int dls_random_prefix(int n, int symmetric, const uint8_t *record, const int32_t *cells, int n_cells,
+                                 uint64_t seed, uint8_t *out_record, double *out_weight) {
+    if (n < 1 || n > DLS_MAX_ORDER || (symmetric && n % 2) || !record || !out_record || !out_weight || n_cells < 0 ||
+        (n_cells && !cells)) {
+        dls::set_error("dls_random_prefix: bad arguments");
+        return DLS_E_ARG;
+    }
+    const int nn = n * n;
+    uint8_t g[DLS_MAX_ORDER * DLS_MAX_ORDER];
+    std::memcpy(g, record, nn);
+    uint32_t rows[DLS_MAX_ORDER] = {}, cols[DLS_MAX_ORDER] = {}, md = 0, ad = 0;
+    for (int c = 0; c < nn; ++c) {
+        const uint8_t v = g[c];
+        if (v == DLS_EMPTY) continue;
+        if (v >= n) { dls::set_error("dls_random_prefix: bad value"); return DLS_E_PREFIX; }
+        const int i = c / n, j = c % n;
+        const uint32_t b = 1u << v;
+        if ((rows[i] & b) || (cols[j] & b) || (i == j && (md & b)) || (i + j == n - 1 && (ad & b))) {
+            dls::set_error("dls_random_prefix: inconsistent record");
+            return DLS_E_PREFIX;
+        }
+        rows[i] |= b; cols[j] |= b;
+        if (i == j) md |= b;
+        if (i + j == n - 1) ad |= b;
+    }
+    uint64_t ctr = seed * 0x9E3779B97F4A7C15ull;
+    auto next = [&]() {   // splitmix64
+        uint64_t z = (ctr += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    };
+    const uint32_t all_n = (1u << n) - 1u;
+    double w = 1.0;
+    for (int k = 0; k < n_cells; ++k) {
+        const int c = cells[k], i = c / n, j = c % n;
+        if (c < 0 || c >= nn || g[c] != DLS_EMPTY) { dls::set_error("dls_random_prefix: bad cell"); return DLS_E_ARG; }
+        const int jm = n - 1 - j;
+        uint32_t cr = rows[i] | cols[j] | (i == j ? md : 0u) | (i + j == n - 1 ? ad : 0u);
+        uint32_t cand = all_n & ~cr;
+        if (symmetric && jm != j) {   // the mirror cell takes n-1-v
+            uint32_t ok = 0;
+            for (int v = 0; v < n; ++v)
+                if ((cand >> v) & 1u) {
+                    const uint32_t m = 1u << (n - 1 - v);
+                    const bool free = !(rows[i] & m) && !(cols[jm] & m) && !(i == jm && (md & m)) &&
+                                      !(i + jm == n - 1 && (ad & m)) && (n - 1 - v) != v;
+                    if (free) ok |= 1u << v;
+                }
+            cand = ok;
+        }
+        const int m = __builtin_popcount(cand);
+        if (m == 0) { *out_weight = 0.0; std::memcpy(out_record, g, nn); return DLS_OK; }
+        w *= m;
+        int pick = (int)(next() % (uint64_t)m);
+        uint32_t b = cand;
+        while (pick--) b &= b - 1;
+        b &= 0u - b;
+        const int v = __builtin_ctz(b);
+        g[c] = (uint8_t)v;
+        rows[i] |= b; cols[j] |= b;
+        if (i == j) md |= b;
+        if (i + j == n - 1) ad |= b;
+        if (symmetric && jm != j) {
+            const uint32_t mb = 1u << (n - 1 - v);
+            g[i * n + jm] = (uint8_t)(n - 1 - v);
+            rows[i] |= mb; cols[jm] |= mb;
+            if (i == jm) md |= mb;
+            if (i + jm == n - 1) ad |= mb;
+        }
+    }
+    *out_weight = w;
+    std::memcpy(out_record, g, nn);
+    return DLS_OK;
+}

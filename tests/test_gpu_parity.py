@@ -329,3 +329,16 @@ def test_count_cells_dls10_paper(k, key):
     g = oracle.first_row_grid(n)
     got, _ = D.dls_count_cells(n, np.where(g < 0, 255, g).astype(np.uint8), list(range(n, k)))
     assert got == paper_counts()[key]
+
+
+def test_monte_carlo_estimate_small_order():
+    """Section 5.3 on the GPU for N = 7, k = 14: the Knuth estimate of the number of
+    DLS with row 0 fixed is within 4 standard errors of the exact count."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("mc", __import__("conftest").ROOT + "/scripts/mc_estimate.py")
+    mc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mc)
+    r = mc.estimate(7, 14, 600, 3)
+    exact = oracle.count_all(7)
+    assert abs(r["knuth"] - exact) < 4 * r["knuth_se"]
+    assert r["N_k"] == oracle.count_prefixes(7, False, oracle.first_row_grid(7), list(range(7, 14)), 7)

@@ -171,3 +171,22 @@ def test_reference_arm_json():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_knuth_descent_unbiased_prefix_count():
+    """Section 5.3 estimator, host half: E[weight] of the random descent over the
+    first k row-major cells = N_n^k, checked against the oracle's exact
+    count within 4 standard errors; deterministic per seed."""
+    n, k = 6, 18
+    g = oracle.first_row_grid(n)
+    rec = np.where(g < 0, 255, g).astype(np.uint8)
+    cells = list(range(n, k))
+    ws = np.array([D.dls_random_prefix(n, rec, cells, s)[1] for s in range(6000)])
+    exact = oracle.count_prefixes(n, False, g, cells, len(cells))
+    assert abs(ws.mean() - exact) < 4 * ws.std() / np.sqrt(len(ws))
+    a, wa = D.dls_random_prefix(n, rec, cells, 77)
+    b, wb = D.dls_random_prefix(n, rec, cells, 77)
+    assert (a == b).all() and wa == wb
+    if wa > 0:
+        full = synth.to_int_grid(a)
+        assert oracle.count(n, False, full)[0] >= 0     # a consistent partial square
