@@ -320,7 +320,6 @@ __device__ __forceinline__ bool load_prefix(const uint8_t *__restrict__ rec, con
 //   then S [L+2][NT] u32, the per-lane stack of Alg. 4's L sets (slot = level+1).
 template <int N, bool VS>
 struct Layout {
-    static constexpr bool BYTES = Geo<N, VS>::BYTES;
     static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT != 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
     // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
     // so the toggle and read parts of a transition share one address register
@@ -383,9 +382,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
 
     const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + LY::BLK_WORDS) + lane;
     const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128 + 4 * lane);
-    const int kBlock = NT;
-    const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte views for t-offsets
-    const char *const Cb = reinterpret_cast<const char *>(Cl);
+    const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte view for t-offsets
 
     uint32_t *const pool = p.pool;
 
@@ -501,7 +498,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     split = (int)(w3 & 0xFFFFu);
                     rest = w3 >> 16;
                     for (int l = 1; l < split; ++l)
-                        S[(l + 1) * kBlock] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
+                        S[(l + 1) * NT] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
                     adopt = true;
                 }
                 __syncwarp();
@@ -515,7 +512,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 uint32_t drest = 0;
                 if (pid >= 0 && lvl > 0) {
                     for (int l = 1; l < lvl && l <= L - p.min_donate; ++l) {
-                        const uint32_t s = S[(l + 1) * kBlock];
+                        const uint32_t s = S[(l + 1) * NT];
                         if (s & (s - 1u)) { dsplit = l; drest = s & (s - 1u); break; }
                     }
                     if (!dsplit && lvl <= L - p.min_donate && (cur & (cur - 1u))) {
@@ -540,11 +537,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     if (recv) {
                         // copy the donor's path above the split level
                         const SW *const Sd = stack + (tid - lane + src);
-                        for (int l = 1; l < d_split; ++l) S[(l + 1) * kBlock] = Sd[(l + 1) * kBlock];
+                        for (int l = 1; l < d_split; ++l) S[(l + 1) * NT] = Sd[(l + 1) * NT];
                     }
                     __syncwarp();
                     if (give) {
-                        if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
+                        if (dsplit < lvl) S[(dsplit + 1) * NT] &= 0u - S[(dsplit + 1) * NT];
                         else cur &= 0u - cur;
                         dsplit = 0;
                     }
@@ -579,13 +576,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                 uint32_t word = 0;
                                 for (int k = 0; k < 8; ++k) {
                                     const int l = 1 + w * 8 + k;
-                                    if (l < dsplit) word |= (uint32_t)(__ffs(S[(l + 1) * kBlock]) - 1) << (4 * k);
+                                    if (l < dsplit) word |= (uint32_t)(__ffs(S[(l + 1) * NT]) - 1) << (4 * k);
                                 }
                                 slot[4 + w] = word;
                             }
                             __threadfence();
                             *(volatile uint32_t *)slot = ticket + 1u;
-                            if (dsplit < lvl) S[(dsplit + 1) * kBlock] &= 0u - S[(dsplit + 1) * kBlock];
+                            if (dsplit < lvl) S[(dsplit + 1) * NT] &= 0u - S[(dsplit + 1) * NT];
                             else cur &= 0u - cur;
                             atomicAdd(acc + 2, 1ull);
                         }
@@ -611,7 +608,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     cur = st.cand(Cl[0]);
                 }
             } else {                           // a donated subtree
-                for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * kBlock], 0u);
+                for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * NT], 0u);
                 lvl = split;
                 cur = rest;
             }
