@@ -41,8 +41,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if build_if_missing and (not os.path.exists(path) or _build._stale()):
+    path = os.environ.get("DLS_LIB", _build.LIB)   # DLS_LIB: alternative build (tuning experiments)
+    if path == _build.LIB and build_if_missing and (not os.path.exists(path) or _build._stale()):
         _build.build()
     if not os.path.exists(path):
         raise DlsError(DLS_E_NODEVICE, "libdls_b200.so is missing: run paper_1709_02599_b200.build")

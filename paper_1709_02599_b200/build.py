@@ -31,12 +31,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    target = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = target + ".tmp%d" % os.getpid()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "--cudart", "static", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+           "--cudart", "static", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include"),
+           *["-D" + d for d in defines], "-o", tmp, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -44,8 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     if verbose:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -46,7 +46,10 @@ namespace {
 typedef unsigned long long u64;
 
 constexpr int kMaxLevels = 100;     // n*n for n = 10
-constexpr int kBurst = 32;          // DFS steps between warp scheduling points
+#ifndef DLS_BURST
+#define DLS_BURST 32
+#endif
+constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Device-wide donation pool (global memory, one per launch): control words
