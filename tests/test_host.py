@@ -190,3 +190,16 @@ def test_knuth_descent_unbiased_prefix_count():
     if wa > 0:
         full = synth.to_int_grid(a)
         assert oracle.count(n, False, full)[0] >= 0     # a consistent partial square
+
+
+def test_cli_host_commands():
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, "-m", "paper_1709_02599_b200", "plan", "--n", "9"], capture_output=True,
+                         text=True, cwd=ROOT)
+    assert out.returncode == 0
+    rows = [list(map(int, l.split())) for l in out.stdout.splitlines()[1:9]]
+    assert (np.array(rows) == fig1()).all()
+    out = subprocess.run([sys.executable, "-m", "paper_1709_02599_b200", "split", "--n", "8", "--depth", "14"],
+                         capture_output=True, text=True, cwd=ROOT)
+    assert out.stdout.strip() == "547896"
