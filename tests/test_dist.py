@@ -68,3 +68,21 @@ def test_two_rank_gloo_count():
     assert all(r[3] == want for r in res)                 # every rank sees the sum
     assert sum(r[2] for r in res) == want                 # shards add up
     assert all(r[4] == 2.0 for r in res)                  # max over ranks
+
+
+def test_bench_split_depth_grows_with_ranks():
+    """bench.py: every rank gets >= ~3.5 workunits per lane (148 SMs x 1024 lanes)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    import paper_1709_02599_b200 as D
+    lib = D.load()
+    prev = 0
+    for world in (1, 2, 4, 8):
+        d = bench.pick_depth(world)
+        assert d >= prev
+        prev = d
+        assert lib.dls_split(8, 0, 1, d, None, 0) >= 3.5 * 148 * 1024 * world
+    assert bench.pick_depth(1) == D.default_split_depth(8)      # config 3: diagonals
