@@ -47,7 +47,7 @@ typedef unsigned long long u64;
 
 constexpr int kMaxLevels = 100;     // n*n for n = 10
 #ifndef DLS_BURST
-#define DLS_BURST 32
+#define DLS_BURST 64
 #endif
 constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
