@@ -140,8 +140,11 @@ int dls_count(int n, int symmetric, int fixed_first_row, int depth,
  *   d_counts       n_prefix uint64 or NULL (zeroed by the call).
  *   d_stats        DLS_STATS_WORDS uint64 (zeroed by the call); after the stream
  *                  completes: [0] total count, [1] search nodes (every cell
- *                  assignment below the records, complete squares included), [2] prefix-error flag
- *                  (nonzero = some record was inconsistent), [3] work-queue
+ *                  assignment below the records, complete squares included), [2] error word
+ *                  (bit 0: some record was inconsistent; bits 8..: internal
+ *                  invariants violated -- only the checked build
+ *                  libdls_b200_checked.so, compiled with -DDLS_CHECKS, sets
+ *                  them; dls_count then returns DLS_E_CUDA), [3] work-queue
  *                  cursor, [4] subtree donations, [5] busy lane-bursts,
  *                  [6] lane-bursts (lane utilisation = [5]/[6]), [7] subtrees
  *                  published to the device-wide donation pool.

@@ -52,6 +52,25 @@ constexpr int kMaxLevels = 100;     // n*n for n = 10
 constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
 constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Internal invariants, compiled in only with -DDLS_CHECKS (the checked build,
+// libdls_b200_checked.so): a violated one sets bit 8 + k of the error word
+// stats[2] (bit 0 stays the prefix-error flag) and the host call fails with
+// DLS_E_CUDA.  The product build compiles them out.
+#ifdef DLS_CHECKS
+#define DLS_CHECK(cond, k) do { if (!(cond)) atomicOr(p.stats + 2, 1ull << (8 + (k))); } while (0)
+#else
+#define DLS_CHECK(cond, k) do { } while (0)
+#endif
+enum CheckBits {
+    kChkStep = 0,       // DFS step: slot / table indices inside levels -1 .. L+1
+    kChkAdopt = 1,      // adopted workunit: pid < n_prefix, split in 0 .. L
+    kChkPoolPut = 2,    // pool producer: slot not still owned by an unread ticket
+    kChkPoolGet = 3,    // pool consumer: pid / split of a claimed slot in range
+    kChkWarpGive = 4,   // intra-warp donation: the source lane really donates
+    kChkExit = 5,       // kernel exit: every lane idle, levels -1 / 0 untouched
+    kChkEmit = 6,       // emitted square: pid in range
+};
 // Device-wide donation pool (global memory, one per launch): control words
 // [0] active warps, [1] waiting warps, [2] head (claimed), [3] tail (reserved),
 // [4] warps registered (exit is allowed only once all warps of the grid are),
@@ -337,6 +356,7 @@ struct Layout {
 template <int N, bool VS, class SW>
 __device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, int NT) {
     typedef Geo<N, VS> G;
+    DLS_CHECK(pid >= 0 && pid < p.n_prefix, kChkEmit);
     const u64 slot = atomicAdd(p.stats + 7, 1ull);
     if ((long long)slot >= p.emit_cap) return;
     uint8_t *dst = p.emit + slot * (u64)(N * N);
@@ -500,6 +520,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     const uint32_t w3 = slot[3];
                     split = (int)(w3 & 0xFFFFu);
                     rest = w3 >> 16;
+                    DLS_CHECK(pid >= 0 && (u64)pid < n_prefix && split >= 1 && 2 * split <= L && rest != 0u,
+                              kChkPoolGet);
                     for (int l = 1; l < split; ++l)
                         S[(l + 1) * NT] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
                     adopt = true;
@@ -537,6 +559,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     const int d_pid = __shfl_sync(kFull, pid, src);
                     const bool recv = pid < 0 && my_rank < pairs;
                     const bool give = dsplit > 0 && dn_rank < pairs;
+                    DLS_CHECK(!recv || ((donors >> src) & 1u && d_split >= 1 && d_split <= L && d_rest != 0u &&
+                                        d_pid >= 0), kChkWarpGive);
                     if (recv) {
                         // copy the donor's path above the split level
                         const SW *const Sd = stack + (tid - lane + src);
@@ -571,7 +595,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                                                              : 0xFFFFFFFFu;
                         const uint32_t best = __reduce_min_sync(kFull, key);
                         if (best != 0xFFFFFFFFu && (best & 31u) == (uint32_t)lane) {
+                            // at most kPoolLimit + (warps in the grid) < kPoolSlots tickets
+                            // can be unreleased: each warp publishes at most one per check
                             const uint32_t ticket = atomicAdd(pool + 3, 1u);
+                            DLS_CHECK(ticket - ld_acquire(pool + 5) < kPoolSlots && 4 + (dsplit + 6) / 8 <= kSlotWords,
+                                      kChkPoolPut);
                             uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
                             slot[1] = (uint32_t)pid;
                             slot[3] = (uint32_t)dsplit | (drest << 16);
@@ -594,6 +622,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             }
         }
         if (adopt) {
+            DLS_CHECK(pid >= 0 && (u64)pid < n_prefix && split >= 0 && split <= L, kChkAdopt);
             // rebuild Rows/Columns from the record, then replay the path
             const bool ok = load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
             cnt = 0;
@@ -634,6 +663,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const uint32_t sibs = sp - bb;                 // L &= L-1
             const uint32_t sb = sibs & (0u - sibs);        // next value of level lvl-1
             const bool mv = !dn && sibs != 0u;             // advance: re-assign level lvl-1
+            DLS_CHECK(lvl >= 0 && lvl <= L + 1 && (!dn || lvl <= L) && (lvl > 0 || (!dn && !mv)), kChkStep);
             if (dn) sl[NT] = cur;                          // push L of level lvl
             if (mv) sl[0] = sibs;
             const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
@@ -667,6 +697,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         if (lane == 0) acc[1] += (u64)wn;
     }
 
+    DLS_CHECK(lvl == 0 && pid < 0 && cnt == 0u && cur == 0u && S[0] == 0u && S[NT] == 0u, kChkExit);
     // ------------------------------------------------ block reduction, 1 atomic per block
     __syncthreads();
     if (tid == 0) {
@@ -874,7 +905,11 @@ bool is_device_ptr(const void *ptr) {
 
 extern "C" int dls_kernel_launches(void) { return 1; }
 
+#ifdef DLS_CHECKS
+extern "C" const char *dls_version(void) { return "dls_b200 0.1.0 sm_100a checked"; }
+#else
 extern "C" const char *dls_version(void) { return "dls_b200 0.1.0 sm_100a"; }
+#endif
 
 extern "C" int dls_count_async(int n, int symmetric, int fixed_first_row, int depth,
                                const uint8_t *d_prefixes, int64_t n_prefix, uint64_t *d_counts,
@@ -919,6 +954,22 @@ struct Workspace {
 Workspace g_ws[64];
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// The kernel's error word stats[2]: bit 0 = an inconsistent prefix record, bits
+// 8.. = violated internal invariants (checked build only, see DLS_CHECK).
+int error_word(u64 w, const char *who) {
+    if (w >> 8) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "%s: internal check failed (mask 0x%llx)", who, (unsigned long long)(w >> 8));
+        dls::set_error(msg);
+        return DLS_E_CUDA;
+    }
+    if (w) {
+        dls::set_error(std::string(who) + ": some prefix record is not a consistent depth-d prefix");
+        return DLS_E_PREFIX;
+    }
+    return DLS_OK;
+}
 
 }  // namespace
 
@@ -1034,10 +1085,7 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     if (out_total) *out_total = stats[0];
     if (out_nodes) *out_nodes = stats[1] + (u64)extra_nodes;
-    if (stats[2] || bad_prefix) {
-        dls::set_error("dls_count: some prefix record is not a consistent depth-d prefix");
-        return DLS_E_PREFIX;
-    }
+    if ((rc = error_word(stats[2] | (bad_prefix ? 1ull : 0ull), "dls_count"))) return rc;
     return DLS_OK;
 }
 
@@ -1080,10 +1128,7 @@ extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth
     cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(d_stats, s);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "dls_emit");
-    if (stats[2]) {
-        dls::set_error("dls_emit: some prefix record is not a consistent depth-d prefix");
-        return DLS_E_PREFIX;
-    }
+    if ((rc = error_word(stats[2], "dls_emit"))) return (int64_t)rc;
     return (int64_t)stats[0];
 }
 

@@ -77,6 +77,14 @@ struct SbParams {
     long long capacity;
 };
 
+// Internal invariants of the checked build (-DDLS_CHECKS): bit 8 + k of
+// counters[2] (bit 0 = canonic-buffer overflow); compiled out otherwise.
+#ifdef DLS_CHECKS
+#define SB_CHECK(cond, k) do { if (!(cond)) atomicOr(p.counters + 2, 1ull << (8 + (k))); } while (0)
+#else
+#define SB_CHECK(cond, k) do { } while (0)
+#endif
+
 __constant__ u64 c_sigma[kMaxGroup / 2];     // sigma as 4-bit fields (index -> image index)
 __constant__ u64 c_sigma_inv[kMaxGroup / 2];
 
@@ -145,6 +153,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
     // D, A from the record; row N-1's assigned cells; column / row masks
     u64 D = 0, A = 0, B = 0;
     uint32_t col[16] = {}, rowL = 0;
+    SB_CHECK(p.k_last >= 0 && p.k_last <= 16 && n <= 16, 0);
     for (int i = 0; i < n; ++i) {
         D |= (u64)rec[i * n + i] << (4 * i);
         A |= (u64)rec[i * n + (n - 1 - i)] << (4 * i);
@@ -152,6 +161,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             const uint8_t v = rec[i * n + j];
+            SB_CHECK(v == DLS_EMPTY || v < n, 1);
             if (v != DLS_EMPTY) col[j] |= 1u << v;
         }
     for (int j = 0; j < n; ++j) {
@@ -219,6 +229,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
             if (lvl + 1 == k) {
                 ++seen;
                 const uint32_t m = canonize_dab(n, p.group, p.mirror_choices, D, A, B);
+                SB_CHECK(m == 0u || (uint32_t)p.group % m == 0u, 2);     // |G| / |Stab|
                 if (m) {
                     ++canon;
                     const unsigned long long slot = atomicAdd(p.counters + 3, 1ull);
@@ -446,6 +457,11 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         cudaMemcpyAsync(cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s);
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) { cleanup(); return fail(e, "hourglass_kernel"); }
         timer.mark("H2D + hourglass kernel", s);
+        if (cnt[2] >> 8) {
+            cleanup();
+            dls::set_error("dls_count_sb: internal check failed (mask " + std::to_string(cnt[2] >> 8) + ")");
+            return DLS_E_CUDA;
+        }
         if (cnt[2]) { cleanup(); dls::set_error("dls_count_sb: canonic buffer overflow"); return DLS_E_ARG; }
         hourglasses += cnt[0];
         classes += cnt[1];
