@@ -41,6 +41,7 @@ SYMMETRIC = False
 WORKLOAD = "dls8_first_row_fixed_full"
 METRIC = "diagonal Latin squares enumerated/sec"
 UNIT = "squares/s"
+NCU_JSON = "r1_ncu_v02.json"   # the committed ncu --set full capture of the timed kernel
 # Algorithmic integer operations per search node: one pass
 # of Alg. 4's loop body for a non-diagonal cell:
 #   CR = Rows|Columns (1), L = AllN^CR (1), L != 0 test (1), b = L&-L (2),
@@ -317,7 +318,7 @@ def main():
         achieved = nodes_l[0] / world * OPS_PER_NODE / (per_launch_ms / 1e3) / 1e12
         ncu = {}
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_ncu_final.json")) as f:
+            with open(os.path.join(ROOT, "profiles", NCU_JSON)) as f:
                 ncu = json.load(f)
         except (OSError, ValueError):
             pass
@@ -335,9 +336,12 @@ def main():
                          "frac": achieved / peak,
                          "traffic": (ncu["dram_read_bytes"] + ncu["dram_write_bytes"]) if ncu else None,
                          "traffic_note": "DRAM bytes per launch from the committed ncu --set full capture "
-                                         "(profiles/r1_ncu_final.json) = the 35 MB of workunit records: the "
-                                         "search itself never touches HBM",
+                                         "(profiles/%s) = the 35 MB of workunit records: the "
+                                         "search itself never touches HBM" % NCU_JSON,
                          "issue_slots_busy_ncu": (ncu.get("issue_slots_busy_pct", 0) / 100.0) if ncu else None,
+                         # the unit that binds the kernel: the shared-memory data pipe
+                         # (table + stack loads), not the integer issue rate
+                         "smem_pipe_busy_ncu": (ncu.get("smem_lsu_wavefronts_pct", 0) / 100.0) if ncu else None,
                          "note": "integer-issue roofline at %.0f MHz (MEASURED_PEAKS sm_max_mhz): 148 SMs x 4 SMSP x "
                                  "32 lanes; achieved = %d algorithmic int ops/node (Alg. 4) x nodes / kernel time"
                                  % (sm_mhz, OPS_PER_NODE)},
