@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -292,6 +293,20 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
     return v;
 }
 
+__device__ __forceinline__ u64 globaltimer() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Timeline stamps (ns, %globaltimer) in the pool header, read back by the host
+// under DLS_TIMING: first warp start, queue found empty, first CTA exit, last
+// CTA exit -- the length of the end-game after the work queue runs dry.
+constexpr int kStampStart = 6, kStampQEmpty = 8, kStampFirstExit = 10, kStampLastExit = 12;
+__device__ __forceinline__ void stamp_first(uint32_t *pool, int w) {
+    atomicCAS(reinterpret_cast<u64 *>(pool + w), 0ull, globaltimer());
+}
+
 __host__ __device__ inline bool pat_bit(const u64 *pat, int c) {
     return (pat[c >> 6] >> (c & 63)) & 1ull;
 }
@@ -431,6 +446,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         atomicAdd(pool + 0, 1u);                   // this warp is active
         __threadfence();
         atomicAdd(pool + 4, 1u);                   // ... and registered
+        stamp_first(pool, kStampStart);
     }
     bool waiting = false;
 
@@ -472,7 +488,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 u64 base = 0;
                 if (lane == leader) base = atomicAdd(p.stats + 3, (u64)__popc(idle));
                 base = __shfl_sync(kFull, base, leader);
-                if (base + (u64)__popc(idle) >= n_prefix) qempty = true;
+                if (base + (u64)__popc(idle) >= n_prefix) {
+                    qempty = true;
+                    if (lane == leader) stamp_first(pool, kStampQEmpty);
+                }
                 if (pid < 0) {
                     const u64 my = base + (u64)__popc(idle & lt_mask);
                     if (my < n_prefix) { pid = (int)my; adopt = true; }
@@ -739,6 +758,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
         atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
         atomicAdd(p.stats + 6, a[4]);   // lane-bursts
         if (!EMIT) atomicMax(p.stats + 7, (u64)ld_acquire(pool + 3));   // subtrees published to the pool
+        stamp_first(pool, kStampFirstExit);
+        atomicMax(reinterpret_cast<u64 *>(pool + kStampLastExit), globaltimer());
     }
 }
 
@@ -907,6 +928,14 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     q.total_warps = (uint32_t)sms * (uint32_t)(nthreads / 32);
     fn<<<(unsigned)sms, nthreads, smem, stream>>>(q);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "kernel launch");
+    if (getenv("DLS_TIMING")) {   // end-game timeline of this launch (synchronises)
+        u64 st[8];
+        cudaMemcpyAsync(st, (uint32_t *)pool + kStampStart, sizeof(st), cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        const double t0 = (double)st[0];
+        fprintf(stderr, "[launch] n_prefix %lld: queue empty at %.1f ms, first CTA exit %.1f ms, last %.1f ms\n",
+                (long long)prm.n_prefix, st[1] ? (st[1] - t0) / 1e6 : -1.0, (st[2] - t0) / 1e6, (st[3] - t0) / 1e6);
+    }
     if ((e = cudaFreeAsync(pool, stream)) != cudaSuccess) return cuda_fail(e, "cudaFreeAsync(pool)");
     return DLS_OK;
 }
@@ -1019,6 +1048,15 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
     Params prm;
     if ((rc = prepare_plan(plan, depth, &prm))) return rc;
     cudaStream_t s = (cudaStream_t)stream;
+    // DLS_TIMING=1: host-side phase times of this call on stderr
+    const bool timing = getenv("DLS_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char *what) {
+        if (!timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[count_records] %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const int nn = n * n;
     const int steps = (int)plan.cells.size();
     cudaError_t e;
@@ -1059,7 +1097,8 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         depth_run = d1;
     }
     const bool refined = depth_run != depth;
-    if (getenv("DLS_TIMING"))   // count_records timing
+    mark("validate + refine");
+    if (timing)
         fprintf(stderr, "[count_records] %lld records at depth %d -> %lld at depth %d\n", (long long)n_prefix, depth,
                 (long long)n_rec, depth_run);
 
@@ -1080,6 +1119,7 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         if ((e = cudaMalloc(&ws.p, cap)) != cudaSuccess) { ws.p = nullptr; return cuda_fail(e, "cudaMalloc(workspace)"); }
         ws.cap = cap;
     }
+    mark("workspace");
     char *const base = (char *)ws.p;
     const uint8_t *d_pre = src;
     if (stage_records) {
@@ -1103,7 +1143,9 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         prm.counts = d_counts;
         prm.parent = refined ? (const uint32_t *)(base + off_par) : nullptr;
         prm.stats = d_stats;
+        mark("H2D + memsets enqueued");
         if ((rc = launch(n, plan.vs, prm, s))) { cudaStreamSynchronize(s); return rc; }
+        mark("launch enqueued");
     }
     u64 stats[DLS_STATS_WORDS];
     if ((e = cudaMemcpyAsync(stats, d_stats, sizeof(stats), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
@@ -1112,6 +1154,7 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
         (e = cudaMemcpyAsync(out_counts, d_counts, (size_t)n_prefix * sizeof(u64), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         return cuda_fail(e, "cudaMemcpyAsync(D2H)");
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    mark("search + D2H (sync)");
     if (out_total) *out_total = stats[0];
     if (out_nodes) *out_nodes = stats[1] + (u64)extra_nodes;
     if ((rc = error_word(stats[2] | (bad_prefix ? 1ull : 0ull), "dls_count"))) return rc;

@@ -21,7 +21,7 @@ def t():
 def main():
     n, d = 8, int(sys.argv[1]) if len(sys.argv) > 1 else 14
     D.count_squares(n, depth=d)          # warm-up (context, module load)
-    for rep in range(3):
+    for rep in range(int(os.environ.get("REPS", "3"))):
         t0 = t()
         lib = B.load()
         total = lib.dls_split(n, 0, 1, d, None, 0)
