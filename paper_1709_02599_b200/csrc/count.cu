@@ -61,6 +61,11 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_CSTRIDE8
 #define DLS_CSTRIDE8 0
 #endif
+// DLS_LAYOUT9: mask layout of DLS N = 9 (2 = 64-bit words + XOR toggles, 3 = three
+//   9-bit fields per 32-bit word + IMAD toggles)
+#ifndef DLS_LAYOUT9
+#define DLS_LAYOUT9 3
+#endif
 #ifndef DLS_ONE_STORE
 #define DLS_ONE_STORE 2
 #endif
@@ -142,7 +147,7 @@ struct Geo {
     static constexpr bool FITS2 = (N + RPW32 - 1) / RPW32 <= 2 && (NC + CPW32 - 1) / CPW32 <= 2;
     // 0: byte fields + PRMT (N <= 8); 1: word fields + funnel shift (e.g. VS N=10);
     // 2: 64-bit words + funnel shifts (DLS N = 9, 10)
-    static constexpr int LAYOUT = N <= 8 ? 0 : (FITS2 ? 1 : 2);
+    static constexpr int LAYOUT = N <= 8 ? 0 : (FITS2 ? 1 : ((N == 9 && !VS && DLS_LAYOUT9 == 3) ? 3 : 2));
     static constexpr bool BYTES = LAYOUT == 0;
     static constexpr int RPW = 64 / RF;                        // layout 2
     static constexpr int CPW = 64 / CF;
@@ -287,6 +292,43 @@ struct Masks<N, VS, 2> {
     typedef uint4 CT;
 };
 
+// DLS N = 9: three 9-bit fields per 32-bit word, R[3] rows and C[3] columns, so
+// a toggle is six IMADs with per-word multipliers (0 for the words without the
+// field; signed deltas never carry between fields, as in the byte layout).
+// Tab: w0..w2 = row-word multipliers of cell(t), w3..w5 = column-word
+//      multipliers, w6 / w7 = row / column selector of cell(t+1): bit offset in
+//      the word (0, 9, 18) | word index << 5.
+template <int N, bool VS>
+struct Masks<N, VS, 3> {
+    typedef Geo<N, VS> G;
+    typedef uint4 CT;
+    static constexpr int FPW = 32 / N;
+    static_assert(!VS && FPW == 3 && (N + FPW - 1) / FPW == 3, "layout 3 is DLS N = 9");
+    uint32_t R[3], C[3];
+
+    __device__ __forceinline__ void clear() { R[0] = R[1] = R[2] = C[0] = C[1] = C[2] = 0; }
+    __device__ __forceinline__ void set_row(int r, uint32_t m) { R[r / FPW] |= m << ((r % FPW) * N); }
+    __device__ __forceinline__ void set_col(int c, uint32_t m) { C[c / FPW] |= m << ((c % FPW) * N); }
+    __device__ __forceinline__ void toggle_d(const uint4 &f, const uint4 &g, uint32_t d) {
+        R[0] += d * f.x;     // IMAD: mark/unmark on the FMA pipe
+        R[1] += d * f.y;
+        R[2] += d * f.z;
+        C[0] += d * f.w;
+        C[1] += d * g.x;
+        C[2] += d * g.y;
+    }
+    __device__ __forceinline__ void toggle(const uint4 &f, const uint4 &g, uint32_t bnew, uint32_t bold) {
+        toggle_d(f, g, bnew - bold);
+    }
+    __device__ __forceinline__ static uint32_t pick(const uint32_t (&a)[3], uint32_t sel) {
+        const uint32_t w = (sel & 64u) ? a[2] : ((sel & 32u) ? a[1] : a[0]);
+        return __funnelshift_r(w, 0u, sel);          // shift by sel & 31
+    }
+    __device__ __forceinline__ uint32_t cand(const uint4 &c) const {
+        return G::ALLN & ~(pick(R, c.z) | pick(C, c.w));
+    }
+};
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -370,13 +412,13 @@ __device__ __forceinline__ bool load_prefix(const uint8_t *__restrict__ rec, con
 //   then S [L+2][NT] u32, the per-lane stack of Alg. 4's L sets (slot = level+1).
 template <int N, bool VS>
 struct Layout {
-    static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT != 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
+    static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT < 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
     // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
     // so the toggle and read parts of a transition share one address register
     static constexpr int BLK_WORDS = 32 * 8;                  // words per transition block
     // stack entries: N <= 16 bit candidate sets; u16 for the 64-bit layout (N = 9,
     // 10 DLS: long searches, so the smaller stack buys 1024 lanes per SM), else u32
-    typedef typename std::conditional<Geo<N, VS>::LAYOUT == 2, uint16_t, uint32_t>::type SW;
+    typedef typename std::conditional<Geo<N, VS>::LAYOUT >= 2, uint16_t, uint32_t>::type SW;
 };
 
 // Rebuild a complete square from the workunit record and the lane's stack and
@@ -677,7 +719,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     cur = st.cand(Cl[0]);
                 }
             } else {                           // a donated subtree
-                for (int l = 1; l < split; ++l) st.toggle(Fl[l * kBlk], S[(l + 1) * NT], 0u);
+                for (int l = 1; l < split; ++l) {
+                    if constexpr (Geo<N, VS>::LAYOUT == 3)
+                        st.toggle(Fl[l * kBlk], Cl[l * kBlk], S[(l + 1) * NT], 0u);
+                    else
+                        st.toggle(Fl[l * kBlk], S[(l + 1) * NT], 0u);
+                }
                 lvl = split;
                 cur = rest;
             }
@@ -713,7 +760,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const char *const tp = Fb + toff;              // one address for both parts
             const uint4 f = *reinterpret_cast<const uint4 *>(tp);
             const CT cs = kCS8 ? *reinterpret_cast<const CT *>(Cb + toff) : *reinterpret_cast<const CT *>(tp + 512);
-            if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
+            if constexpr (Geo<N, VS>::LAYOUT == 3) {
+                st.toggle_d(f, cs, dn ? b : sb - bb);                             // mark / unmark
+            } else if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
                 st.toggle(f, dn ? b : sb, dn ? 0u : bb);                          // mark / unmark
             } else {
                 const uint32_t d = dn ? b : sb - bb;                              // mark / unmark
@@ -795,7 +844,7 @@ int layout_of(int n, bool vs) {
     const int rf = vs ? (h > 0 ? h : 1) : n, cf = n, nc = vs ? h : n;
     const int rpw32 = 32 / rf, cpw32 = 32 / cf;
     const bool fits2 = (n + rpw32 - 1) / rpw32 <= 2 && (nc + cpw32 - 1) / cpw32 <= 2;
-    return n <= 8 ? 0 : (fits2 ? 1 : 2);
+    return n <= 8 ? 0 : (fits2 ? 1 : ((n == 9 && !vs && DLS_LAYOUT9 == 3) ? 3 : 2));
 }
 
 void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
@@ -818,6 +867,9 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             } else if (lay == 1) {
                 (i / rpw32 == 0 ? e.w[0] : e.w[1]) = 1u << ((i % rpw32) * rf);
                 (j / cpw32 == 0 ? e.w[2] : e.w[3]) = 1u << ((j % cpw32) * cf);
+            } else if (lay == 3) {
+                e.w[i / 3] = 1u << ((i % 3) * n);
+                e.w[3 + j / 3] = 1u << ((j % 3) * n);
             } else {
                 e.w[0] = (uint32_t)((i % rpw) * rf);
                 e.w[1] = (uint32_t)(i / rpw);
@@ -836,6 +888,9 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             } else if (lay == 1) {
                 e.w[4] = (uint32_t)(32 * (i / rpw32) + (i % rpw32) * rf);
                 e.w[5] = (uint32_t)(32 * (j / cpw32) + (j % cpw32) * cf);
+            } else if (lay == 3) {
+                e.w[6] = (uint32_t)((i % 3) * n) | (uint32_t)(i / 3) << 5;
+                e.w[7] = (uint32_t)((j % 3) * n) | (uint32_t)(j / 3) << 5;
             } else {
                 e.w[4] = (uint32_t)((i % rpw) * rf);
                 e.w[5] = (uint32_t)(i / rpw);
@@ -895,7 +950,7 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
 }
 
 size_t smem_bytes(int n, bool vs, int L, int nthreads) {
-    const size_t sw = layout_of(n, vs) == 2 ? 2 : 4;
+    const size_t sw = layout_of(n, vs) >= 2 ? 2 : 4;
     return (size_t)(L + 2) * 32 * 32 + (size_t)(L + 2) * nthreads * sw;
 }
 
@@ -913,7 +968,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     const int lay = layout_of(n, vs);
     int nthreads = 1024;                   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
-    while (lay == 2 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
+    while (lay >= 2 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
     const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)

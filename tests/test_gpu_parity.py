@@ -262,20 +262,21 @@ def test_repeatable():
     assert (a[0] == b[0]).all() and a[1:] == b[1:]
 
 
-@pytest.mark.parametrize("n,vs,k", [(7, False, 3), (8, False, 2), (8, True, 5), (10, True, 1)])
+@pytest.mark.parametrize("n,vs,k", [(7, False, 3), (8, False, 2), (8, True, 5), (10, True, 1), (9, False, 2)])
 def test_few_workunits_spread_by_device_pool(n, vs, k):
     """dls_count_async does no host refinement: k workunits start on k lanes and
     reach the rest of the GPU only through warp donation and the device-wide pool."""
     import torch
     d = D.default_split_depth(n, vs)
-    if n == 10:
-        recs = synth.diagonal_prefixes(synth.SEED_VS10, n, 3, vs=True)
+    if n >= 9:
+        recs = synth.diagonal_prefixes(synth.SEED_VS10 if vs else synth.SEED_DLS9, n, 3, vs=vs)
         recs = recs[:k]
-        # deepen by one row so the oracle finishes in seconds
+        # deepen (VS10: one row; DLS9: two rows) so the oracle finishes in seconds
+        extra = 6 if vs else 14
         order = oracle.plan(n, vs)
-        kids = oracle.prefixes(n, vs, synth.to_int_grid(recs[0]), order[d:], 6)
+        kids = oracle.prefixes(n, vs, synth.to_int_grid(recs[0]), order[d:], extra)
         recs = np.where(kids[:k] < 0, 255, kids[:k]).astype(np.uint8)
-        d += 6
+        d += extra
     else:
         recs = D.dls_split(n, d, vs)
         rng = np.random.default_rng(n)
@@ -312,7 +313,7 @@ def test_emit_squares_equal_oracle(n, vs, fixed):
     assert D.dls_emit(n, d, recs, small, vs, fixed) == total               # capacity < total
 
 
-@pytest.mark.parametrize("n,vs,k", [(7, False, 21), (8, False, 26), (8, True, 24), (6, False, 20)])
+@pytest.mark.parametrize("n,vs,k", [(7, False, 21), (8, False, 26), (8, True, 24), (6, False, 20), (9, False, 22)])
 def test_count_cells_row_major_vs_oracle(n, vs, k):
     """N_n^k: consistent assignments of the first k row-major cells, row 0 fixed."""
     g = oracle.first_row_grid(n)
