@@ -52,22 +52,17 @@ constexpr int kMaxLevels = 100;     // n*n for n = 10
 #endif
 constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 // Shared-memory wavefronts bound the byte-layout kernel (ncu: LSU data pipe at
-// 98% of peak), so two switches trade a few ALU instructions for wavefronts:
-// DLS_CSTRIDE8: 8-byte read entries get their own 8-byte lane stride (no 2-way
-//   bank conflict; one more address IMAD per step);
-// DLS_ONE_STORE: the push (descend) and the rewrite (advance) of a stack slot
-//   are one predicated store: 1 = with a selected address, 2 = at slot nl (the
-//   slot both write, and the one the next step loads).
-#ifndef DLS_CSTRIDE8
-#define DLS_CSTRIDE8 0
-#endif
+// 97-98% of peak).  DLS_ONE_STORE=1 (default): the push (descend, slot lvl+1)
+// and the rewrite (advance, slot lvl) of a stack slot are one predicated store
+// at slot nl -- the slot both write and the one the next step loads; 0 = two
+// predicated stores (A/B baseline).
 // DLS_LAYOUT9: mask layout of DLS N = 9 (2 = 64-bit words + XOR toggles, 3 = three
 //   9-bit fields per 32-bit word + IMAD toggles)
 #ifndef DLS_LAYOUT9
 #define DLS_LAYOUT9 3
 #endif
 #ifndef DLS_ONE_STORE
-#define DLS_ONE_STORE 2
+#define DLS_ONE_STORE 1
 #endif
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
 constexpr unsigned kFull = 0xFFFFFFFFu;
@@ -448,7 +443,6 @@ dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
     typedef Layout<N, VS> LY;
-    constexpr bool kCS8 = DLS_CSTRIDE8 && sizeof(CT) == 8;    // byte layout read entries
     extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
     const int NT = LY::NT_FIXED ? LY::NT_FIXED : (int)blockDim.x;
@@ -462,10 +456,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         const Tab &e = p.tab[k >> 5];
         uint32_t *const blk = smem + (k >> 5) * LY::BLK_WORDS;
         reinterpret_cast<uint4 *>(blk)[k & 31] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
-        if constexpr (kCS8)
-            reinterpret_cast<uint2 *>(blk + 128)[k & 31] = make_uint2(e.w[4], e.w[5]);
-        else
-            reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+        reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
@@ -478,9 +469,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
     constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
 
     const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + LY::BLK_WORDS) + lane;
-    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128 + (kCS8 ? 2 : 4) * lane);
+    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128 + 4 * lane);
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte view for t-offsets
-    const char *const Cb = reinterpret_cast<const char *>(Cl);
 
     uint32_t *const pool = p.pool;
 
@@ -748,18 +738,14 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const uint32_t sb = sibs & (0u - sibs);        // next value of level lvl-1
             const bool mv = !dn && sibs != 0u;             // advance: re-assign level lvl-1
             DLS_CHECK(lvl >= 0 && lvl <= L + 1 && (!dn || lvl <= L) && (lvl > 0 || (!dn && !mv)), kChkStep);
-            if constexpr (DLS_ONE_STORE == 1) {
-                SW *const dst = dn ? sl + NT : sl;
-                const uint32_t val = dn ? cur : sibs;
-                if (dn || mv) *dst = (SW)val;              // push L of level lvl / L &= L-1
-            } else if constexpr (DLS_ONE_STORE == 0) {
+            if constexpr (!DLS_ONE_STORE) {
                 if (dn) sl[NT] = cur;                      // push L of level lvl
                 if (mv) sl[0] = sibs;
             }
             const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
             const char *const tp = Fb + toff;              // one address for both parts
             const uint4 f = *reinterpret_cast<const uint4 *>(tp);
-            const CT cs = kCS8 ? *reinterpret_cast<const CT *>(Cb + toff) : *reinterpret_cast<const CT *>(tp + 512);
+            const CT cs = *reinterpret_cast<const CT *>(tp + 512);
             if constexpr (Geo<N, VS>::LAYOUT == 3) {
                 st.toggle_d(f, cs, dn ? b : sb - bb);                             // mark / unmark
             } else if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
@@ -773,7 +759,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const int nl = max(t + (adv ? 1 : 0), 0);
             // level L+1 is virtual: reaching it completes a square (P:93
             // SquaresCnt++); its "cell" reads full row/column fields, so c = 0 there
-            if constexpr (DLS_ONE_STORE == 2) {
+            if constexpr (DLS_ONE_STORE) {
                 // the slot a push (slot lvl+1) or an advance (slot lvl) writes is
                 // slot nl in both cases: the address the next step loads from
                 if (adv) S[nl * NT] = (SW)(dn ? cur : sibs);
