@@ -56,10 +56,13 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 // and the rewrite (advance, slot lvl) of a stack slot are one predicated store
 // at slot nl -- the slot both write and the one the next step loads; 0 = two
 // predicated stores (A/B baseline).
-// DLS_LAYOUT9: mask layout of DLS N = 9 (2 = 64-bit words + XOR toggles, 3 = three
-//   9-bit fields per 32-bit word + IMAD toggles)
+// DLS_LAYOUT9 / DLS_LAYOUT10: mask layout of DLS N = 9 / 10 (2 = 64-bit words +
+//   XOR toggles; 3 / 4 = three 9- / 10-bit fields per 32-bit word + IMAD toggles)
 #ifndef DLS_LAYOUT9
 #define DLS_LAYOUT9 3
+#endif
+#ifndef DLS_LAYOUT10
+#define DLS_LAYOUT10 4
 #endif
 #ifndef DLS_ONE_STORE
 #define DLS_ONE_STORE 1
@@ -142,7 +145,10 @@ struct Geo {
     static constexpr bool FITS2 = (N + RPW32 - 1) / RPW32 <= 2 && (NC + CPW32 - 1) / CPW32 <= 2;
     // 0: byte fields + PRMT (N <= 8); 1: word fields + funnel shift (e.g. VS N=10);
     // 2: 64-bit words + funnel shifts (DLS N = 9, 10)
-    static constexpr int LAYOUT = N <= 8 ? 0 : (FITS2 ? 1 : ((N == 9 && !VS && DLS_LAYOUT9 == 3) ? 3 : 2));
+    static constexpr int LAYOUT = N <= 8 ? 0
+                                : FITS2 ? 1
+                                : (N == 9 && !VS && DLS_LAYOUT9 == 3) ? 3
+                                : (N == 10 && !VS && DLS_LAYOUT10 == 4) ? 4 : 2;
     static constexpr bool BYTES = LAYOUT == 0;
     static constexpr int RPW = 64 / RF;                        // layout 2
     static constexpr int CPW = 64 / CF;
@@ -321,6 +327,49 @@ struct Masks<N, VS, 3> {
     }
     __device__ __forceinline__ uint32_t cand(const uint4 &c) const {
         return G::ALLN & ~(pick(R, c.z) | pick(C, c.w));
+    }
+};
+
+// DLS N = 10: three 10-bit fields per 32-bit word.  Rows 1..9 in R[3] (row r at
+// word (r-1)/3), columns 0..8 in C[3], and X = column 9 (offset 0) | row 0
+// (offset 10): seven IMAD toggles (a cell of row 0 or column 9 has a multiplier
+// on X; cell (0, 9) has 1 + 2^10 there).  Tab: w0..w2 = R multipliers, w3..w5 =
+// C multipliers, w6 = X multiplier, w7 = row selector | column selector << 16
+// (selector = bit offset | word << 5, word 3 = X).
+template <int N, bool VS>
+struct Masks<N, VS, 4> {
+    typedef Geo<N, VS> G;
+    typedef uint4 CT;
+    static_assert(!VS && N == 10, "layout 4 is DLS N = 10");
+    uint32_t R[3], C[3], X;
+
+    __device__ __forceinline__ void clear() { R[0] = R[1] = R[2] = C[0] = C[1] = C[2] = X = 0; }
+    __device__ __forceinline__ void set_row(int r, uint32_t m) {
+        if (r == 0) X |= m << N;
+        else R[(r - 1) / 3] |= m << (((r - 1) % 3) * N);
+    }
+    __device__ __forceinline__ void set_col(int c, uint32_t m) {
+        if (c == N - 1) X |= m;
+        else C[c / 3] |= m << ((c % 3) * N);
+    }
+    __device__ __forceinline__ void toggle_d(const uint4 &f, const uint4 &g, uint32_t d) {
+        R[0] += d * f.x;     // IMAD: mark/unmark on the FMA pipe
+        R[1] += d * f.y;
+        R[2] += d * f.z;
+        C[0] += d * f.w;
+        C[1] += d * g.x;
+        C[2] += d * g.y;
+        X += d * g.z;
+    }
+    __device__ __forceinline__ void toggle(const uint4 &f, const uint4 &g, uint32_t bnew, uint32_t bold) {
+        toggle_d(f, g, bnew - bold);
+    }
+    __device__ __forceinline__ static uint32_t pick(const uint32_t (&a)[3], uint32_t x, uint32_t sel) {
+        const uint32_t w = (sel & 64u) ? ((sel & 32u) ? x : a[2]) : ((sel & 32u) ? a[1] : a[0]);
+        return __funnelshift_r(w, 0u, sel);          // shift by sel & 31
+    }
+    __device__ __forceinline__ uint32_t cand(const uint4 &c) const {
+        return G::ALLN & ~(pick(R, X, c.w) | pick(C, X, c.w >> 16));
     }
 };
 
@@ -710,7 +759,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 }
             } else {                           // a donated subtree
                 for (int l = 1; l < split; ++l) {
-                    if constexpr (Geo<N, VS>::LAYOUT == 3)
+                    if constexpr (Geo<N, VS>::LAYOUT >= 3)
                         st.toggle(Fl[l * kBlk], Cl[l * kBlk], S[(l + 1) * NT], 0u);
                     else
                         st.toggle(Fl[l * kBlk], S[(l + 1) * NT], 0u);
@@ -746,7 +795,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const char *const tp = Fb + toff;              // one address for both parts
             const uint4 f = *reinterpret_cast<const uint4 *>(tp);
             const CT cs = *reinterpret_cast<const CT *>(tp + 512);
-            if constexpr (Geo<N, VS>::LAYOUT == 3) {
+            if constexpr (Geo<N, VS>::LAYOUT >= 3) {
                 st.toggle_d(f, cs, dn ? b : sb - bb);                             // mark / unmark
             } else if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
                 st.toggle(f, dn ? b : sb, dn ? 0u : bb);                          // mark / unmark
@@ -830,7 +879,10 @@ int layout_of(int n, bool vs) {
     const int rf = vs ? (h > 0 ? h : 1) : n, cf = n, nc = vs ? h : n;
     const int rpw32 = 32 / rf, cpw32 = 32 / cf;
     const bool fits2 = (n + rpw32 - 1) / rpw32 <= 2 && (nc + cpw32 - 1) / cpw32 <= 2;
-    return n <= 8 ? 0 : (fits2 ? 1 : ((n == 9 && !vs && DLS_LAYOUT9 == 3) ? 3 : 2));
+    return n <= 8 ? 0
+         : fits2 ? 1
+         : (n == 9 && !vs && DLS_LAYOUT9 == 3) ? 3
+         : (n == 10 && !vs && DLS_LAYOUT10 == 4) ? 4 : 2;
 }
 
 void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
@@ -856,6 +908,11 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             } else if (lay == 3) {
                 e.w[i / 3] = 1u << ((i % 3) * n);
                 e.w[3 + j / 3] = 1u << ((j % 3) * n);
+            } else if (lay == 4) {
+                if (i == 0) e.w[6] += 1u << n;
+                else e.w[(i - 1) / 3] = 1u << (((i - 1) % 3) * n);
+                if (j == n - 1) e.w[6] += 1u;
+                else e.w[3 + j / 3] = 1u << ((j % 3) * n);
             } else {
                 e.w[0] = (uint32_t)((i % rpw) * rf);
                 e.w[1] = (uint32_t)(i / rpw);
@@ -877,6 +934,10 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             } else if (lay == 3) {
                 e.w[6] = (uint32_t)((i % 3) * n) | (uint32_t)(i / 3) << 5;
                 e.w[7] = (uint32_t)((j % 3) * n) | (uint32_t)(j / 3) << 5;
+            } else if (lay == 4) {
+                const uint32_t rs = i == 0 ? (uint32_t)n | 3u << 5 : (uint32_t)(((i - 1) % 3) * n) | (uint32_t)((i - 1) / 3) << 5;
+                const uint32_t cs = j == n - 1 ? 3u << 5 : (uint32_t)((j % 3) * n) | (uint32_t)(j / 3) << 5;
+                e.w[7] = rs | cs << 16;
             } else {
                 e.w[4] = (uint32_t)((i % rpw) * rf);
                 e.w[5] = (uint32_t)(i / rpw);

@@ -313,7 +313,7 @@ def test_emit_squares_equal_oracle(n, vs, fixed):
     assert D.dls_emit(n, d, recs, small, vs, fixed) == total               # capacity < total
 
 
-@pytest.mark.parametrize("n,vs,k", [(7, False, 21), (8, False, 26), (8, True, 24), (6, False, 20), (9, False, 22)])
+@pytest.mark.parametrize("n,vs,k", [(7, False, 21), (8, False, 26), (8, True, 24), (6, False, 20), (9, False, 22), (10, False, 20)])
 def test_count_cells_row_major_vs_oracle(n, vs, k):
     """N_n^k: consistent assignments of the first k row-major cells, row 0 fixed."""
     g = oracle.first_row_grid(n)
