@@ -18,7 +18,7 @@ import pytest
 from conftest import ROOT
 
 SELECT = ("config1 or config2 or config3_dls8_full or config4_vs8 or small_orders or empty or ragged "
-          "or inconsistent or device_buffers or few_workunits or emit or count_cells_row_major "
+          "or inconsistent or device_buffers or few_workunits or pool_stress or emit or count_cells_row_major "
           "or gpu_canonize_all or gpu_count_sb")
 
 

@@ -262,6 +262,37 @@ def test_repeatable():
     assert (a[0] == b[0]).all() and a[1:] == b[1:]
 
 
+@pytest.mark.parametrize("n,vs,k,reps", [(8, False, 1, 12), (8, False, 4, 8), (8, True, 6, 8)])
+def test_pool_stress_repeated_launches(n, vs, k, reps):
+    """The device-wide pool under contention: the k largest of 40 seeded
+    workunits (no host refinement) spread over all 148 x 1024 lanes, launched
+    `reps` times on one stream.  Every launch must give the oracle's
+    per-workunit counts and node total; a torn or lost donated subtree would
+    show as a count or node difference."""
+    import torch
+    d = D.default_split_depth(n, vs)
+    recs = D.dls_split(n, d, vs)
+    rng = np.random.default_rng(100 + n + vs)
+    pool = np.ascontiguousarray(recs[rng.choice(len(recs), 40, replace=False)])
+    sizes = [_oracle_per_prefix(n, vs, pool[i:i + 1], d)[1] for i in range(len(pool))]
+    recs = np.ascontiguousarray(pool[np.argsort(sizes)[::-1][:k]])
+    want, want_nodes = _oracle_per_prefix(n, vs, recs, d)
+    dev = torch.from_numpy(recs).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    outs = [torch.zeros(k, dtype=torch.int64, device="cuda") for _ in range(reps)]
+    stats = [torch.zeros(B.DLS_STATS_WORDS, dtype=torch.int64, device="cuda") for _ in range(reps)]
+    for o, st in zip(outs, stats):
+        D.dls_count_async(n, d, dev, o, st, vs, stream=s)
+    torch.cuda.synchronize()
+    donated = 0
+    for o, st in zip(outs, stats):
+        st = st.cpu().tolist()
+        assert (o.cpu().numpy().astype(np.uint64) == want).all()
+        assert st[2] == 0 and st[0] == int(want.sum()) and st[1] == want_nodes
+        donated += st[4]
+    assert donated > 0                       # the pool / donation path really ran
+
+
 @pytest.mark.parametrize("n,vs,k", [(7, False, 3), (8, False, 2), (8, True, 5), (10, True, 1), (9, False, 2)])
 def test_few_workunits_spread_by_device_pool(n, vs, k):
     """dls_count_async does no host refinement: k workunits start on k lanes and
