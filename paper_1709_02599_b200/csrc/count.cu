@@ -984,6 +984,7 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     prm->donate = 1;
     prm->min_donate = std::max(kMinDonateDepth, prm->L / 3);
     if (const char *e = getenv("DLS_DONATE")) prm->donate = atoi(e);   // 0: no donation (diagnostics)
+    if (const char *e = getenv("DLS_MIN_DONATE")) prm->min_donate = std::max(1, atoi(e));   // tuning
     return DLS_OK;
 }
 
