@@ -1,4 +1,7 @@
-"""Small runs of every kernel, for compute-sanitizer (one tool per call)."""
+"""Small runs of every kernel (search, device pool, emit, hourglass + canonise,
+symmetry breaking, cells).  compute-sanitizer is closed on the GPU pool; run this
+with DLS_LIB=paper_1709_02599_b200/libdls_b200_checked.so to exercise the
+kernels' own invariants (DLS_CHECK) instead."""
 import os
 import sys
 
