@@ -1002,23 +1002,6 @@ size_t smem_bytes(int n, bool vs, int L, int nthreads) {
     return (size_t)(L + 2) * 32 * 32 + (size_t)(L + 2) * nthreads * sw;
 }
 
-// The donation pool comes from the device's default stream-ordered memory pool.
-// With its default release threshold (0) every synchronisation hands the freed
-// 2 MB back to the OS, and now and then that costs 0.25-0.5 s after the kernel
-// has finished (profiles/r1_e2e_variance.log).  Keep up to 64 MB cached instead
-// (once per device; DLS_POOL_KEEP=0 restores the default for A/B).
-void keep_pool_memory(int dev) {
-    static std::once_flag once[64];
-    std::call_once(once[dev & 63], [dev]() {
-        const char *e = getenv("DLS_POOL_KEEP");
-        if (e && atoi(e) == 0) return;
-        cudaMemPool_t mp;
-        if (cudaDeviceGetDefaultMemPool(&mp, dev) != cudaSuccess) { cudaGetLastError(); return; }
-        uint64_t keep = 64ull << 20;
-        if (cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) cudaGetLastError();
-    });
-}
-
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
@@ -1041,7 +1024,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     // one CTA per SM even for few workunits: warps without a workunit start by
     // taking donated subtrees from the device-wide pool
     void *pool = nullptr;
-    keep_pool_memory(dev);
+    dls::keep_pool_memory(dev);
     if ((e = cudaMallocAsync(&pool, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(pool)");
     if ((e = cudaMemsetAsync(pool, 0, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(pool)");
     Params q = prm;
@@ -1154,6 +1137,24 @@ int error_word(u64 w, const char *who) {
 
 
 namespace dls {
+
+// The donation pool comes from the device's default stream-ordered memory pool.
+// With its default release threshold (0) every synchronisation hands the freed
+// 2 MB back to the OS, and now and then that costs 0.25-1.2 s after the kernel
+// has finished (profiles/r1_e2e_variance.log).  Keep up to 1 GB cached instead
+// (the symmetry-breaking driver's scratch comes from the same pool; once per
+// device; DLS_POOL_KEEP=0 restores the default for A/B).
+void keep_pool_memory(int dev) {
+    static std::once_flag once[64];
+    std::call_once(once[dev & 63], [dev]() {
+        const char *e = getenv("DLS_POOL_KEEP");
+        if (e && atoi(e) == 0) return;
+        cudaMemPool_t mp;
+        if (cudaDeviceGetDefaultMemPool(&mp, dev) != cudaSuccess) { cudaGetLastError(); return; }
+        uint64_t keep = 1ull << 30;
+        if (cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) cudaGetLastError();
+    });
+}
 
 // dls_count for an arbitrary plan (the standard one, or the hourglass plan of
 // the symmetry-broken driver).

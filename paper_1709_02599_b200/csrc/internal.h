@@ -47,6 +47,8 @@ bool valid_record(const Plan &plan, int depth, const uint8_t *rec);
 // dls_count for an arbitrary plan (count.cu).
 // Records are refined on the host (P:481 below each record) when fewer than
 // refine_below (< 0: the default, ~1 per lane) are given.
+// Keep freed memory of the device's default stream-ordered pool cached (once).
+void keep_pool_memory(int dev);
 int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
                   uint64_t *out_total, uint64_t *out_nodes, void *stream, int64_t refine_below = -1);
 

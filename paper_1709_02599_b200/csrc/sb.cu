@@ -425,15 +425,18 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
     unsigned long long *d_cnt = nullptr;
     cudaError_t e;
     auto cleanup = [&]() {
-        cudaFree(d_diag);
-        cudaFree(d_rec);
-        cudaFree(d_mult);
-        cudaFree(d_cnt);
+        for (void *q : {(void *)d_diag, (void *)d_rec, (void *)d_mult, (void *)d_cnt})
+            if (q) cudaFreeAsync(q, s);
+        cudaStreamSynchronize(s);
     };
-    if ((e = cudaMalloc(&d_diag, (size_t)std::min<int64_t>(n_diag, chunk) * nn + 1)) != cudaSuccess ||
-        (e = cudaMalloc(&d_rec, (size_t)cap * nn)) != cudaSuccess ||
-        (e = cudaMalloc(&d_mult, (size_t)cap * 4)) != cudaSuccess ||
-        (e = cudaMalloc(&d_cnt, 4 * sizeof(unsigned long long))) != cudaSuccess) {
+    // scratch from the stream-ordered pool (kept cached across calls)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dls::keep_pool_memory(dev);
+    if ((e = cudaMallocAsync((void **)&d_diag, (size_t)std::min<int64_t>(n_diag, chunk) * nn + 1, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void **)&d_rec, (size_t)cap * nn, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void **)&d_mult, (size_t)cap * 4, s)) != cudaSuccess ||
+        (e = cudaMallocAsync((void **)&d_cnt, 4 * sizeof(unsigned long long), s)) != cudaSuccess) {
         cleanup();
         return fail(e, "cudaMalloc");
     }
