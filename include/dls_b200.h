@@ -34,6 +34,10 @@
  * Error behaviour: every call returns a negative DLS_E_* code on failure and
  * writes nothing it did not document as written.  No call aborts the process.
  * Thread safety: calls are reentrant; dls_count serialises on its own stream.
+ * Device memory: per-launch scratch (the 2 MB donation pool, the symmetry-breaking
+ * buffers) comes from the device's default stream-ordered memory pool; on first
+ * use the library sets that pool's release threshold to 1 GB so freed scratch
+ * stays cached between calls (DLS_POOL_KEEP=0 in the environment skips this).
  */
 #ifndef DLS_B200_H
 #define DLS_B200_H

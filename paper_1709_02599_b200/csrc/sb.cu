@@ -355,23 +355,31 @@ extern "C" int dls_canonize(int n, int symmetric, const uint8_t *hourglasses, in
     uint32_t *d_out = out_mult;
     void *tmp_in = nullptr, *tmp_out = nullptr;
     const size_t bytes = (size_t)n_rec * n * n;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dls::keep_pool_memory(dev);
     if (!device_ptr(hourglasses)) {
-        if ((e = cudaMalloc(&tmp_in, bytes)) != cudaSuccess) return fail(e, "cudaMalloc");
+        if ((e = cudaMallocAsync(&tmp_in, bytes, s)) != cudaSuccess) return fail(e, "cudaMallocAsync");
         cudaMemcpyAsync(tmp_in, hourglasses, bytes, cudaMemcpyHostToDevice, s);
         d_in = (const uint8_t *)tmp_in;
     }
     const bool host_out = !device_ptr(out_mult);
     if (host_out) {
-        if ((e = cudaMalloc(&tmp_out, (size_t)n_rec * 4)) != cudaSuccess) { cudaFree(tmp_in); return fail(e, "cudaMalloc"); }
+        if ((e = cudaMallocAsync(&tmp_out, (size_t)n_rec * 4, s)) != cudaSuccess) {
+            if (tmp_in) cudaFreeAsync(tmp_in, s);
+            cudaStreamSynchronize(s);
+            return fail(e, "cudaMallocAsync");
+        }
         d_out = (uint32_t *)tmp_out;
     }
     canonize_kernel<<<(unsigned)((n_rec + kSbThreads - 1) / kSbThreads), kSbThreads, 0, s>>>(d_in, n_rec, n, group,
                                                                                              mirrors, d_out);
     e = cudaGetLastError();
     if (e == cudaSuccess && host_out) e = cudaMemcpyAsync(out_mult, d_out, (size_t)n_rec * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (tmp_in) cudaFree(tmp_in);
-    if (tmp_out) cudaFree(tmp_out);
+    if (tmp_in) cudaFreeAsync(tmp_in, s);
+    if (tmp_out) cudaFreeAsync(tmp_out, s);
+    const cudaError_t es = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = es;
     return e == cudaSuccess ? DLS_OK : fail(e, "dls_canonize");
 }
 
