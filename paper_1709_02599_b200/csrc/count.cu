@@ -16,13 +16,17 @@
 //    mark its next candidate in ONE toggle: Alg. 4's "L &= L-1" then "LS = L & -L")
 //    and  backtrack; all busy lanes of a warp execute the same instructions;
 //  * per-level candidate sets (Alg. 4's L[i][j]) live in a per-lane stack in
-//    shared memory, u32 per level, layout [level][lane] (bank-conflict free);
+//    shared memory, u32 (u16 for N = 9, 10 DLS) per level, layout [level][lane]
+//    (bank-conflict free);
 //    the lowest set bit of a stacked L is the value assigned at that level;
 //  * Rows/Columns occupancy sets are bit fields in registers.  N <= 8: byte fields
 //    in 32-bit words -- a cell's candidates are two PRMT byte-selects and one LOP3,
 //    marks/unmarks are IMADs with per-cell power-of-two multipliers (FMA pipe,
-//    leaving the ALU pipe to the control flow).  N = 9, 10: 64-bit words with
-//    funnel shifts.  Per-transition geometry comes pre-decoded from a table;
+//    leaving the ALU pipe to the control flow).  VS N = 10: fields in two words
+//    per set, funnel-shift reads.  DLS N = 9, 10: three 9/10-bit fields per
+//    word, IMAD toggles, word-select + funnel-shift reads (layouts 3, 4; the
+//    64-bit-word layout 2 is kept as their A/B baseline).  Per-transition
+//    geometry comes pre-decoded from a table;
 //  * a global atomic work queue hands prefixes to lanes (one atomic per warp
 //    refill); once it is drained, idle lanes receive the untried siblings of the
 //    shallowest open level of a busy lane of their warp (warp-vote donation);
@@ -144,7 +148,8 @@ struct Geo {
     static constexpr int CPW32 = 32 / CF;
     static constexpr bool FITS2 = (N + RPW32 - 1) / RPW32 <= 2 && (NC + CPW32 - 1) / CPW32 <= 2;
     // 0: byte fields + PRMT (N <= 8); 1: word fields + funnel shift (e.g. VS N=10);
-    // 2: 64-bit words + funnel shifts (DLS N = 9, 10)
+    // 2: 64-bit words + funnel shifts (A/B baseline); 3 / 4: three 9 / 10-bit
+    // fields per word + IMAD toggles (DLS N = 9 / 10)
     static constexpr int LAYOUT = N <= 8 ? 0
                                 : FITS2 ? 1
                                 : (N == 9 && !VS && DLS_LAYOUT9 == 3) ? 3
@@ -245,8 +250,8 @@ struct Masks<N, VS, 1> {
     }
 };
 
-// N = 9, 10: row/column fields packed in 64-bit words (W of them), moved by
-// funnel shifts.  Tab: w0..w3 = row shift, row word, col shift, col word of
+// 64-bit words (the A/B baseline of DLS N = 9, 10): row/column fields packed in
+// W words, moved by funnel shifts.  Tab: w0..w3 = row shift, row word, col shift, col word of
 // cell(t); w4..w7 = the same of cell(t+1).
 template <int N, bool VS>
 struct Masks<N, VS, 2> {
@@ -460,8 +465,8 @@ struct Layout {
     // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
     // so the toggle and read parts of a transition share one address register
     static constexpr int BLK_WORDS = 32 * 8;                  // words per transition block
-    // stack entries: N <= 16 bit candidate sets; u16 for the 64-bit layout (N = 9,
-    // 10 DLS: long searches, so the smaller stack buys 1024 lanes per SM), else u32
+    // stack entries: N <= 16 bit candidate sets; u16 for layouts 2-4 (DLS N = 9,
+    // 10: long searches, so the smaller stack buys 1024 lanes per SM), else u32
     typedef typename std::conditional<Geo<N, VS>::LAYOUT >= 2, uint16_t, uint32_t>::type SW;
 };
 
