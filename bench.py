@@ -41,7 +41,7 @@ SYMMETRIC = False
 WORKLOAD = "dls8_first_row_fixed_full"
 METRIC = "diagonal Latin squares enumerated/sec"
 UNIT = "squares/s"
-NCU_JSON = "r1_ncu_v02.json"   # the committed ncu --set full capture of the timed kernel
+NCU_JSON = "r1_ncu_b256.json"   # the committed ncu --set full capture of the timed kernel
 # Algorithmic integer operations per search node: one pass
 # of Alg. 4's loop body for a non-diagonal cell:
 #   CR = Rows|Columns (1), L = AllN^CR (1), L != 0 test (1), b = L&-L (2),

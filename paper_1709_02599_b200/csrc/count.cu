@@ -52,7 +52,7 @@ typedef unsigned long long u64;
 
 constexpr int kMaxLevels = 100;     // n*n for n = 10
 #ifndef DLS_BURST
-#define DLS_BURST 64
+#define DLS_BURST 256
 #endif
 constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 // Shared-memory wavefronts bound the byte-layout kernel (ncu: LSU data pipe at
