@@ -28,8 +28,8 @@
  *                  (the GPU search then only tracks row and column sets).
  *   count          number of complete (symmetric) DLS that extend a prefix.
  *   node           a consistent partial square visited below a prefix (each
- *                  successful cell assignment, leaves included); the unit of
- *                  "search nodes/sec".
+ *                  successful cell assignment of the searched levels, see
+ *                  dls_search_levels); the unit of "search nodes/sec".
  *
  * Error behaviour: every call returns a negative DLS_E_* code on failure and
  * writes nothing it did not document as written.  No call aborts the process.
@@ -136,6 +136,20 @@ int dls_count(int n, int symmetric, int fixed_first_row, int depth,
               const uint8_t *prefix_buf, int64_t n_prefix,
               uint64_t *out_counts, uint64_t *out_total, uint64_t *out_nodes,
               void *stream);
+
+/*
+ * dls_search_levels -- number of plan cells the GPU search assigns below a
+ * depth-`depth` record: n_steps - depth, or fewer when the two-row closure applies
+ * (DESIGN.md "Tail closure"): at the first level after which only two rows have
+ * empty cells, in the same columns and off both diagonals, the search stops and
+ * counts the completions in closed form (GF(2) rank of the columns' missing
+ * pairs).  The nodes dls_count reports are the assignments of these levels
+ * (R15).  The environment variable DLS_CLOSE=0 turns the closure off
+ * (full search; diagnostics and A/B).
+ *   out_levels     host int32.
+ * Returns DLS_OK or DLS_E_ARG.
+ */
+int dls_search_levels(int n, int symmetric, int fixed_first_row, int depth, int32_t *out_levels);
 
 /*
  * dls_count_async -- the same search, enqueued on `stream` without waiting.

@@ -54,6 +54,8 @@ def _load():
         ull = ctypes.POINTER(ctypes.c_ulonglong)
         lib.oracle_count.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ull, ull]
         lib.oracle_count.restype = ctypes.c_int
+        lib.oracle_count_levels.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ull, ull]
+        lib.oracle_count_levels.restype = ctypes.c_int
         lib.oracle_prefixes.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ip, ctypes.c_longlong]
         lib.oracle_prefixes.restype = ctypes.c_longlong
         lib.oracle_squares.argtypes = [ctypes.c_int, ctypes.c_int, ip, ip, ctypes.c_int, ip, ctypes.c_longlong]
@@ -135,6 +137,24 @@ def count(n: int, vs: bool, grid: np.ndarray, order: Optional[Sequence[int]] = N
     if rc != 0:
         raise ValueError("oracle_count failed: %d" % rc)
     return int(c.value), int(nd.value)
+
+
+def count_levels(n: int, vs: bool, grid: np.ndarray, order: Optional[Sequence[int]] = None) -> Tuple[int, List[int]]:
+    """(completions, nodes per depth) of a partial square: entry k counts the
+    consistent assignments of the first k+1 cells of ``order`` (R9, R15)."""
+    grid = np.asarray(grid).reshape(n, n)
+    if order is None:
+        order = plan_for_grid(n, vs, grid)
+    g, gp = _iarr(grid.reshape(-1))
+    o, op = _iarr(list(order) if len(order) else [0])
+    lv = (ctypes.c_ulonglong * max(len(order), 1))()
+    c = ctypes.c_ulonglong(0)
+    rc = _load().oracle_count_levels(n, int(bool(vs)), gp, op, len(order), ctypes.byref(c), lv)
+    if rc == -2:
+        return 0, [0] * len(order)
+    if rc != 0:
+        raise ValueError("oracle_count_levels failed: %d" % rc)
+    return int(c.value), [int(lv[k]) for k in range(len(order))]
 
 
 def count_all(n: int, vs: bool = False, fixed_first_row: bool = True) -> int:

@@ -20,6 +20,7 @@
  *   oracle_count     -- number of completions of a partial square in a given order
  *                       (Alg. 1/2, with explicit scans instead of the
  *                       occupancy arrays), plus the number of search nodes
+ *   oracle_count_levels -- the same, with the nodes split by depth
  *   oracle_prefixes  -- all consistent assignments of the first `depth` cells of an
  *                       order (workunit decomposition)
  *   oracle_squares   -- writes out every completion (for square-by-square checks)
@@ -57,6 +58,7 @@ typedef struct {
     int canon;                    /* 1: at the stop depth canonise (Alg. 5) instead of emitting */
     long long classes;            /* canonical designs found */
     long long *mult_out;          /* their class sizes (up to emit_cap) */
+    unsigned long long *level_nodes; /* optional: nodes per depth (assignments of order[k]) */
 } oracle_state;
 
 long long oracle_canonize(int n, int vs, const int *g);
@@ -150,6 +152,7 @@ static void fill(oracle_state *s, int step)
     for (v = 0; v < s->n; v++) {
         if (!place(s, i, j, v)) continue;
         s->nodes++;
+        if (s->level_nodes) s->level_nodes[step]++;
         fill(s, step + 1);
         unplace(s, i, j);
     }
@@ -191,6 +194,26 @@ int oracle_count(int n, int vs, const int *grid, const int *order, int n_order,
     if (rc == 0) fill(s, 0);
     if (count) *count = rc == 0 ? s->count : 0;
     if (nodes) *nodes = rc == 0 ? s->nodes : 0;
+    free(s);
+    return rc;
+}
+
+/* oracle_count with the nodes split by depth: level_nodes[k] (k < n_order) =
+ * number of successful assignments of order[k], i.e. of consistent partial
+ * squares that assign exactly the first k+1 cells of the order (R9:
+ * a node is one successful assignment).  Summing level_nodes[0..d-1] gives the
+ * nodes of the search truncated after d cells (R15). */
+int oracle_count_levels(int n, int vs, const int *grid, const int *order, int n_order,
+                        unsigned long long *count, unsigned long long *level_nodes)
+{
+    oracle_state *s = (oracle_state *)malloc(sizeof(oracle_state));
+    int rc = load(s, n, vs, grid, order, n_order), k;
+    for (k = 0; k < n_order; k++) level_nodes[k] = 0;
+    s->level_nodes = level_nodes;
+    if (rc == 0) fill(s, 0);
+    if (count) *count = rc == 0 ? s->count : 0;
+    if (rc != 0)
+        for (k = 0; k < n_order; k++) level_nodes[k] = 0;
     free(s);
     return rc;
 }

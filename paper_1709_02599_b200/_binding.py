@@ -21,7 +21,7 @@ DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
            "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_count_cells",
-           "dls_random_prefix", "dls_kernel_launches")
+           "dls_random_prefix", "dls_kernel_launches", "dls_search_levels")
 
 _lib = None
 
@@ -73,6 +73,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_random_prefix.argtypes = [c_int, c_int, vp, vp, c_int, ctypes.c_uint64, vp, vp]
     lib.dls_random_prefix.restype = c_int
     lib.dls_kernel_launches.restype = c_int
+    lib.dls_search_levels.argtypes = [c_int, c_int, c_int, c_int, vp]
+    lib.dls_search_levels.restype = c_int
     _lib = lib
     return lib
 
@@ -232,6 +234,15 @@ def dls_random_prefix(n: int, record: np.ndarray, cells, seed: int, symmetric: b
                                   ctypes.c_uint64(seed & (2 ** 64 - 1)), out.ctypes.data, ctypes.addressof(w))
     _check(rc, "dls_random_prefix")
     return out.reshape(n, n), float(w.value)
+
+
+def dls_search_levels(n: int, depth: int, symmetric: bool = False, fixed_first_row: bool = True) -> int:
+    """Plan cells the GPU search assigns below depth-`depth` records (the two-row
+    closure level, or n_steps - depth); the reported nodes are their assignments."""
+    out = ctypes.c_int32(0)
+    rc = load().dls_search_levels(n, int(symmetric), int(fixed_first_row), depth, ctypes.addressof(out))
+    _check(rc, "dls_search_levels")
+    return int(out.value)
 
 
 def dls_kernel_launches() -> int:

@@ -126,6 +126,21 @@ struct Params {
     uint32_t total_warps;    // warps of the grid (exit once all registered)
     uint8_t *emit;           // emit kernels: complete squares, n*n bytes each
     long long emit_cap;      //               capacity (records)
+    // two-row closure: the search stops at level L,
+    // where only rows r1, r2 still have empty cells, all in the same columns and
+    // off both diagonals; the completions of such a state are counted in closed
+    // form from the column sets and row r1 (close_count)
+    int close;               // 1: level L+1 is a closure event (CLOSE kernels)
+    uint32_t cl_open;        // tracked columns with empty cells in rows r1, r2
+    int cl_E;                // popc(cl_open)
+    int cl_rword;            // mask-layout word holding row r1's field
+    int cl_rshift;           // bit offset of row r1's field in that word
+    uint32_t cl_sel[10];     // field selectors of the columns of J (padded)
+    // forced cells just before the two-row level, assigned inside the closure
+    // (their value is the one candidate their complete-but-one row or column
+    // leaves): read entry (words 4..7) and toggle entry (words 0..7) of each
+    int cl_nf;
+    Tab cl_fread[2], cl_ftog[2];
     uint8_t level_cell[kMaxLevels + 2];   // cell (i*n+j) of level l = 1..L
     Tab tab[kMaxLevels + 2]; // tab[t + 1], t = -1 .. L
 };
@@ -378,6 +393,217 @@ struct Masks<N, VS, 4> {
     }
 };
 
+// ---------------------------------------------------------------- two-row closure
+//
+// At the closure level every row except r1, r2 is complete, the empty cells of
+// r1 and r2 lie in the same columns J and on neither diagonal.  Each column j in
+// J then misses exactly two values e_j, and a value v is missing from
+// m1(v) + m2(v) columns of J (m_r(v) = 1 if row r misses v; counting argument,
+// DESIGN.md "Tail closure").  A completion is a choice p_j in e_j for row r1
+// (row r2 takes the other value) such that row r1 receives each of its missing
+// values once; with the degrees above this is exactly the GF(2) condition
+//     XOR_j p_j = M1   <=>   XOR_{j: x_j = 1} e_j = t,
+//     t = M1 ^ XOR_j low(e_j)      (x_j = 1: row r1 takes the higher value),
+// whose number of solutions is 2^(|J| - rank) if t lies in the span of the e_j
+// and 0 otherwise.  Row r2 is then complete and valid by the same counting.
+// Vertical symmetry: the same over the N/2 value pairs {v, N-1-v} of the left
+// columns, e_j = fold(missing positions) (a column missing both values of one
+// pair gives e_j = 0: two completions that differ in that column).
+//
+// A closure event stores the part of the state it needs (the column words and
+// the words holding row r1) in its lane's queue in shared memory; the warp
+// evaluates 32 queued events at a time, one per lane (Close::eval).  The host
+// lists the columns of J as layout-specific field selectors (cl_sel), padded to
+// EM entries with a complete column (its missing set is empty).
+template <int N, bool VS, int LAYOUT = Geo<N, VS>::LAYOUT>
+struct Close;
+
+template <int N, bool VS>
+struct CloseBase {
+    typedef Geo<N, VS> G;
+    static constexpr uint32_t RMASK = VS ? G::HMASK : G::ALLN;
+    // |J| <= EM: rows r1 != r2 close >= 2 diagonal columns (DLS) / >= 1 left one (VS)
+    static constexpr int EM = VS ? (G::H > 1 ? G::H - 1 : 1) : (N > 2 ? N - 2 : 1);
+    __device__ __forceinline__ static uint32_t fold(uint32_t m) { return VS ? (m ^ (m >> G::H)) & G::HMASK : m; }
+    // f[k]: field of the k-th column of J (occupied values / positions)
+    __device__ __forceinline__ static uint32_t count(const uint32_t (&f)[EM], uint32_t rowf, const Params &p) {
+        uint32_t e[EM];
+        uint32_t x = 0;
+#pragma unroll
+        for (int k = 0; k < EM; ++k) {
+            const uint32_t m = G::ALLN & ~f[k];        // the two values column k misses
+            x ^= m & (0u - m);                         // XOR_j low(e_j)
+            e[k] = fold(m);
+        }
+        uint32_t t = fold(x) ^ (RMASK & ~rowf);        // M1 ^ XOR_j low(e_j)
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < EM; ++k) {                 // Gaussian elimination over GF(2)
+            const uint32_t ek = e[k];
+            const uint32_t piv = ek & (0u - ek);
+            rank += ek != 0u;
+#pragma unroll
+            for (int j = k + 1; j < EM; ++j)
+                if (e[j] & piv) e[j] ^= ek;
+            if (t & piv) t ^= ek;
+        }
+        return t ? 0u : 1u << (p.cl_E - rank);
+    }
+};
+
+// byte layout: queue entry {C0, C1, R0, R1}; column selector = byte index
+template <int N, bool VS>
+struct Close<N, VS, 0> : CloseBase<N, VS> {
+    typedef CloseBase<N, VS> B;
+    static constexpr int EW = 4;   // words per queue entry
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t) {
+        return make_uint4(st.C0, st.C1, st.R0, st.R1);
+    }
+    __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
+        uint4 w = *reinterpret_cast<const uint4 *>(src);
+        bool ok = true;
+        if (p.cl_nf) {
+            Masks<N, VS> m;
+            m.C0 = w.x; m.C1 = w.y; m.R0 = w.z; m.R1 = w.w;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (k < p.cl_nf) {
+                    const uint32_t v = m.cand(make_uint2(p.cl_fread[k].w[4], p.cl_fread[k].w[5]));
+                    ok &= v != 0u;
+                    m.toggle(make_uint4(p.cl_ftog[k].w[0], p.cl_ftog[k].w[1], p.cl_ftog[k].w[2], p.cl_ftog[k].w[3]), v, 0u);
+                }
+            w = make_uint4(m.C0, m.C1, m.R0, m.R1);
+        }
+        uint32_t f[B::EM];
+#pragma unroll
+        for (int k = 0; k < B::EM; ++k) f[k] = prmt(w.x, w.y, p.cl_sel[k]) & 0xFFu;
+        const uint32_t c = B::count(f, ((rsel ? w.w : w.z) >> p.cl_rshift) & 0xFFu, p);
+        return ok ? c : 0u;
+    }
+};
+
+// word fields (VS N = 10): entry {C0, C1, R0, R1}; selector = bit offset of the
+// field in the 64-bit pair C1:C0
+template <int N, bool VS>
+struct Close<N, VS, 1> : CloseBase<N, VS> {
+    typedef CloseBase<N, VS> B;
+    typedef Geo<N, VS> G;
+    static constexpr int EW = 4;
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t) {
+        return make_uint4(st.C0, st.C1, st.R0, st.R1);
+    }
+    __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
+        uint4 w = *reinterpret_cast<const uint4 *>(src);
+        bool ok = true;
+        if (p.cl_nf) {
+            Masks<N, VS> m;
+            m.C0 = w.x; m.C1 = w.y; m.R0 = w.z; m.R1 = w.w;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (k < p.cl_nf) {
+                    const Tab &rd = p.cl_fread[k], &tg = p.cl_ftog[k];
+                    const uint32_t v = m.cand(make_uint4(rd.w[4], rd.w[5], rd.w[6], rd.w[7]));
+                    ok &= v != 0u;
+                    m.toggle(make_uint4(tg.w[0], tg.w[1], tg.w[2], tg.w[3]), v, 0u);
+                }
+            w = make_uint4(m.C0, m.C1, m.R0, m.R1);
+        }
+        uint32_t f[B::EM];
+#pragma unroll
+        for (int k = 0; k < B::EM; ++k)
+            f[k] = (uint32_t)((((u64)w.y << 32) | w.x) >> p.cl_sel[k]) & ((1u << G::CF) - 1u);
+        const uint32_t c = B::count(f, ((rsel ? w.w : w.z) >> p.cl_rshift) & ((1u << G::RF) - 1u), p);
+        return ok ? c : 0u;
+    }
+};
+
+// DLS N = 9: entry {C0, C1, C2, word of row r1}; selector = bit offset | word
+// << 5 (as the read entries of layout 3)
+template <int N, bool VS>
+struct Close<N, VS, 3> : CloseBase<N, VS> {
+    typedef CloseBase<N, VS> B;
+    static constexpr int EW = 4;
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t rsel) {
+        const uint32_t rw = rsel == 2 ? st.R[2] : (rsel == 1 ? st.R[1] : st.R[0]);
+        return make_uint4(st.C[0], st.C[1], st.C[2], rw);
+    }
+    __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
+        uint4 w = *reinterpret_cast<const uint4 *>(src);
+        bool ok = true;
+        if (p.cl_nf) {   // the forced cells' rows share row r1's word (host check)
+            Masks<N, VS, 3> m;
+            m.C[0] = w.x; m.C[1] = w.y; m.C[2] = w.z;
+            m.R[0] = rsel == 0 ? w.w : 0u; m.R[1] = rsel == 1 ? w.w : 0u; m.R[2] = rsel == 2 ? w.w : 0u;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (k < p.cl_nf) {
+                    const Tab &rd = p.cl_fread[k], &tg = p.cl_ftog[k];
+                    const uint32_t v = m.cand(make_uint4(rd.w[4], rd.w[5], rd.w[6], rd.w[7]));
+                    ok &= v != 0u;
+                    m.toggle(make_uint4(tg.w[0], tg.w[1], tg.w[2], tg.w[3]), make_uint4(tg.w[4], tg.w[5], tg.w[6], tg.w[7]),
+                             v, 0u);
+                }
+            w = make_uint4(m.C[0], m.C[1], m.C[2], rsel == 2 ? m.R[2] : (rsel == 1 ? m.R[1] : m.R[0]));
+        }
+        const uint32_t c[3] = {w.x, w.y, w.z};
+        uint32_t f[B::EM];
+#pragma unroll
+        for (int k = 0; k < B::EM; ++k) f[k] = Masks<N, VS, 3>::pick(c, p.cl_sel[k]) & 0x1FFu;
+        const uint32_t cnt = B::count(f, (w.w >> p.cl_rshift) & 0x1FFu, p);
+        return ok ? cnt : 0u;
+    }
+};
+
+// DLS N = 10: entry {C0, C1, C2, X} + the word of row r1 (two stores, 20 of the
+// slot's 32 bytes); selector as the read entries of layout 4
+template <int N, bool VS>
+struct Close<N, VS, 4> : CloseBase<N, VS> {
+    typedef CloseBase<N, VS> B;
+    static constexpr int EW = 8;
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t) {
+        return make_uint4(st.C[0], st.C[1], st.C[2], st.X);
+    }
+    __device__ __forceinline__ static uint32_t pack_row(const Masks<N, VS> &st, uint32_t rsel) {
+        return rsel == 3 ? st.X : (rsel == 2 ? st.R[2] : (rsel == 1 ? st.R[1] : st.R[0]));
+    }
+    __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
+        uint4 w = *reinterpret_cast<const uint4 *>(src);
+        uint32_t rw = src[4];
+        bool ok = true;
+        if (p.cl_nf) {   // the forced cells' rows share row r1's word (host check)
+            Masks<N, VS, 4> m;
+            m.C[0] = w.x; m.C[1] = w.y; m.C[2] = w.z; m.X = w.w;
+            m.R[0] = rsel == 0 ? rw : 0u; m.R[1] = rsel == 1 ? rw : 0u; m.R[2] = rsel == 2 ? rw : 0u;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                if (k < p.cl_nf) {
+                    const Tab &rd = p.cl_fread[k], &tg = p.cl_ftog[k];
+                    const uint32_t v = m.cand(make_uint4(rd.w[4], rd.w[5], rd.w[6], rd.w[7]));
+                    ok &= v != 0u;
+                    m.toggle(make_uint4(tg.w[0], tg.w[1], tg.w[2], tg.w[3]), make_uint4(tg.w[4], tg.w[5], tg.w[6], tg.w[7]),
+                             v, 0u);
+                }
+            w = make_uint4(m.C[0], m.C[1], m.C[2], m.X);
+            rw = rsel == 3 ? m.X : (rsel == 2 ? m.R[2] : (rsel == 1 ? m.R[1] : m.R[0]));
+        }
+        const uint32_t c[3] = {w.x, w.y, w.z};
+        uint32_t f[B::EM];
+#pragma unroll
+        for (int k = 0; k < B::EM; ++k) f[k] = Masks<N, VS, 4>::pick(c, w.w, p.cl_sel[k]) & 0x3FFu;
+        const uint32_t cnt = B::count(f, (rw >> p.cl_rshift) & 0x3FFu, p);
+        return ok ? cnt : 0u;
+    }
+};
+
+// layout 2 (the 64-bit A/B baseline) has no closure: the host never enables it
+template <int N, bool VS>
+struct Close<N, VS, 2> : CloseBase<N, VS> {
+    static constexpr int EW = 4;
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &, uint32_t) { return make_uint4(0, 0, 0, 0); }
+    __device__ __forceinline__ static uint32_t pack_row(const Masks<N, VS> &, uint32_t) { return 0u; }
+    __device__ __forceinline__ static uint32_t eval(const uint32_t *, const Params &, uint32_t) { return 0u; }
+};
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -465,10 +691,24 @@ struct Layout {
     // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
     // so the toggle and read parts of a transition share one address register
     static constexpr int BLK_WORDS = 32 * 8;                  // words per transition block
-    // stack entries: N <= 16 bit candidate sets; u16 for layouts 2-4 (DLS N = 9,
-    // 10: long searches, so the smaller stack buys 1024 lanes per SM), else u32
-    typedef typename std::conditional<Geo<N, VS>::LAYOUT >= 2, uint16_t, uint32_t>::type SW;
+    // stack entries: the candidate sets of one level, u8 for N <= 8 (layout 0),
+    // else u16.  PACK entries share a 32-bit word: entry (slot s, lane t) is byte
+    // s * NT * sizeof(SW) + 4 t + sizeof(SW) * (t / (NT / PACK)), so the lanes of a
+    // warp always touch 32 different banks (whatever their levels) and slot s of a
+    // lane is still element s * NT of an SW array based at the lane's offset
+    typedef typename std::conditional<Geo<N, VS>::LAYOUT == 0, uint8_t, uint16_t>::type SW;
+    static constexpr int PACK = 4 / (int)sizeof(SW);
+    // closure queue (CLOSE kernels): CQ entries per lane, [slot][lane]; the warp
+    // checks the queues every GROUP steps and drains them all once some queue
+    // holds more than CQ - GROUP entries, so none can overflow
+    static constexpr int CQ = Geo<N, VS>::LAYOUT == 0 ? 9 : (Geo<N, VS>::LAYOUT == 1 ? 7 : 6);
+    static constexpr int GROUP = Geo<N, VS>::LAYOUT == 0 ? 6 : 4;
+    static_assert(CQ > GROUP, "closure queue too small");
 };
+
+__host__ __device__ inline uint32_t stack_lane_offset(int t, int nt, int sw) {
+    return 4u * (uint32_t)t + (uint32_t)sw * (uint32_t)(t / (nt / (4 / sw)));
+}
 
 // Rebuild a complete square from the workunit record and the lane's stack and
 // append it to p.emit (the optional compact emit of squares for small N).
@@ -491,12 +731,14 @@ __device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, 
     }
 }
 
-template <int N, bool VS, bool EMIT>
+
+template <int N, bool VS, bool EMIT, bool CLOSE>
 __global__ void __launch_bounds__(1024, 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
     typedef Layout<N, VS> LY;
+    typedef Close<N, VS> CL;
     extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
     const int NT = LY::NT_FIXED ? LY::NT_FIXED : (int)blockDim.x;
@@ -504,7 +746,24 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     typedef typename LY::SW SW;
-    SW *const stack = reinterpret_cast<SW *>(smem + (L + 2) * LY::BLK_WORDS);
+    char *const stk = reinterpret_cast<char *>(smem + (L + 2) * LY::BLK_WORDS);
+    // closure queues ([slot][lane], Close::EW words per entry) and the per-lane
+    // completion counters they feed, after the stack (16-byte aligned)
+    const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)NT * (uint32_t)sizeof(SW);
+    char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
+    const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per queue slot
+    uint32_t *const lanecnt = reinterpret_cast<uint32_t *>(cq_mem + LY::CQ * CQSTR);
+    const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
+    const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * (uint32_t)CL::EW * 4u;
+    uint32_t cq_w = cq_lane0;          // shared address of this lane's next queue entry
+    int cq_n = 0, cq_r = 0;            // entries written / evaluated since the queue was last empty
+    // (with a compile-time lane count cq_n is recomputed from cq_w at the checks)
+    constexpr bool kCqShift = LY::NT_FIXED != 0;
+    constexpr int kCqLog = LY::NT_FIXED == 1024 ? (CL::EW == 4 ? 14 : 15) : 0;
+    static_assert(!kCqShift || (1 << kCqLog) == LY::NT_FIXED * CL::EW * 4, "queue slot stride");
+    uint32_t cq_rot = 0;               // first lane of the next pass (round robin)
+    const uint32_t rsel = (uint32_t)p.cl_rword;
+    if (CLOSE) lanecnt[tid] = 0u;
 
     for (int k = tid; k < (L + 2) * 32; k += NT) {
         const Tab &e = p.tab[k >> 5];
@@ -514,11 +773,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
-    stack[tid] = 0u;
-    stack[NT + tid] = 0u;
-    __syncthreads();
     // slot of level l (l = -1 .. L): S[(l + 1) * NT]
-    SW *const S = stack + tid;
+    SW *const S = reinterpret_cast<SW *>(stk + stack_lane_offset(tid, NT, (int)sizeof(SW)));
+    S[0] = 0u;
+    S[NT] = 0u;
+    __syncthreads();
     // transition t: Fl[t * kBlk] (toggle part), Cl at +512 bytes (read part)
     constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
 
@@ -553,8 +812,64 @@ dls_search_kernel(const __grid_constant__ Params p) {
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
+    // Evaluate up to 32 pending closure events of this warp, the oldest of each
+    // lane first, one per lane: lane i takes the i-th event of the concatenation
+    // of the lanes' queues (exclusive prefix sums + a binary search over them),
+    // credits the completions to the lane that raised it, and every lane drops
+    // the events taken from its queue (an emptied queue restarts at slot 0).
+    auto close_pass = [&]() {
+        const int c = cq_n - cq_r;
+        // lanes in round-robin order starting at cq_rot, so that no queue waits long
+        const int rl = (lane - (int)cq_rot) & 31;           // rank of this lane
+        int inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_sync(kFull, inc, (lane - d) & 31);
+            if (rl >= d) inc += v;
+        }
+        const int pex = inc - c;
+        const int total = __shfl_sync(kFull, inc, (int)(cq_rot + 31u) & 31);
+        int sr = 0;                                          // rank of the source lane
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            const int v = __shfl_sync(kFull, pex, (sr + d + (int)cq_rot) & 31);
+            if (v <= lane) sr += d;
+        }
+        const int src = (sr + (int)cq_rot) & 31;
+        const int s_pex = __shfl_sync(kFull, pex, src);
+        const uint32_t s_addr = __shfl_sync(kFull, cq_lane0 + (uint32_t)cq_r * CQSTR, src);
+        __syncwarp();
+        if (lane < total) {
+            const uint32_t *e = reinterpret_cast<const uint32_t *>(
+                cq_mem + (s_addr - cq_sa) + (uint32_t)(lane - s_pex) * CQSTR);
+            const uint32_t k = CL::eval(e, p, rsel);
+            if (k) atomicAdd(lanecnt + (tid - lane) + src, k);
+        }
+        __syncwarp();
+        cq_r += max(0, min(32 - pex, c));
+        if (cq_r == cq_n) { cq_r = cq_n = 0; cq_w = cq_lane0; }
+        cq_rot = (cq_rot + 7u) & 31u;
+        return total;
+    };
+    auto close_drain = [&]() {
+        while (__reduce_add_sync(kFull, (unsigned)(cq_n - cq_r)) != 0u) close_pass();
+    };
+
     for (;;) {
         // ------------------------------------------------ scheduling point
+        if (CLOSE) {
+            // every pending event belongs to the lane's current workunit: settle
+            // them before a lane can finish it or take another
+            close_drain();
+            __syncwarp();
+            cnt += lanecnt[tid];
+            lanecnt[tid] = 0u;
+            if (pid >= 0 && cnt >= 0x80000000u) {
+                if (p.counts) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
+                atomicAdd(acc + 0, (u64)cnt);
+                cnt = 0;
+            }
+        }
         if (pid >= 0 && lvl == 0) {
             if (p.counts && cnt) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
             if (cnt) atomicAdd(acc + 0, (u64)cnt);
@@ -686,7 +1001,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                         d_pid >= 0), kChkWarpGive);
                     if (recv) {
                         // copy the donor's path above the split level
-                        const SW *const Sd = stack + (tid - lane + src);
+                        const SW *const Sd = reinterpret_cast<const SW *>(stk + stack_lane_offset(tid - lane + src, NT, (int)sizeof(SW)));
                         for (int l = 1; l < d_split; ++l) S[(l + 1) * NT] = Sd[(l + 1) * NT];
                     }
                     __syncwarp();
@@ -780,8 +1095,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if (lane == 0) { acc[3] += (u64)__popc(busy); acc[4] += 32; }
         }
         uint32_t cnt32 = 0, ent32 = 0;
-#pragma unroll 8
-        for (int s = 0; s < kBurst; ++s) {
+        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? LY::GROUP : 8)) {
+#pragma unroll
+        for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
             const bool dn = cur != 0u;                     // descend: cell(lvl) has candidates
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
             const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
@@ -818,11 +1134,44 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 // slot nl in both cases: the address the next step loads from
                 if (adv) S[nl * NT] = (SW)(dn ? cur : sibs);
             }
-            cnt32 += nl > L ? 1u : 0u;
+            if (!CLOSE) cnt32 += nl > L ? 1u : 0u;
             if (EMIT && nl > L) emit_square<N, VS, SW>(p, pid, S, NT);
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
             lvl = nl;
+            if constexpr (CLOSE) {
+                // level L+1 is a closure event: append the state to the lane's
+                // queue -- two predicated instructions, no branch, no vote
+                const uint4 w = CL::pack(st, rsel);
+                if constexpr (Geo<N, VS>::LAYOUT != 4) {
+                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %0, %1;\n\t"
+                                 "@ev st.shared.v4.u32 [%2], {%3, %4, %5, %6};\n\t}"
+                                 :: "r"(nl), "r"(L), "r"(cq_w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w));
+                } else {
+                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %0, %1;\n\t"
+                                 "@ev st.shared.v4.u32 [%2], {%3, %4, %5, %6};\n\t"
+                                 "@ev st.shared.u32 [%2+16], %7;\n\t}"
+                                 :: "r"(nl), "r"(L), "r"(cq_w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w),
+                                    "r"(CL::pack_row(st, rsel)));
+                }
+                const bool ev = nl > L;
+                cq_w += ev ? CQSTR : 0u;
+                if constexpr (!kCqShift) cq_n += ev ? 1 : 0;
+            }
+        }
+            if constexpr (CLOSE) {
+                // evaluate full batches of 32; drain everything when some queue
+                // could overflow during the next group.  One reduction carries
+                // both: the pending events (< 1024) and 1024 per queue near full.
+                if constexpr (kCqShift) cq_n = (int)((cq_w - cq_lane0) >> kCqLog);
+                const unsigned pk = (unsigned)(cq_n - cq_r) + (cq_n > LY::CQ - LY::GROUP ? 1024u : 0u);
+                const unsigned red = __reduce_add_sync(kFull, pk);
+                if (red >= 1024u) {
+                    close_drain();
+                } else if (red >= 32u) {
+                    close_pass();
+                }
+            }
         }
         cnt += cnt32;
         if (cnt >= 0x80000000u) {          // flush before 32 bits could overflow
@@ -855,20 +1204,23 @@ dls_search_kernel(const __grid_constant__ Params p) {
 typedef void (*KernelFn)(Params);
 
 template <int N, bool VS>
-KernelFn kernel_for(bool emit) { return emit ? dls_search_kernel<N, VS, true> : dls_search_kernel<N, VS, false>; }
+KernelFn kernel_for(bool emit, bool close) {
+    return emit ? dls_search_kernel<N, VS, true, false>
+                : (close ? dls_search_kernel<N, VS, false, true> : dls_search_kernel<N, VS, false, false>);
+}
 
-KernelFn pick_kernel(int n, bool vs, bool emit) {
+KernelFn pick_kernel(int n, bool vs, bool emit, bool close) {
     switch (n) {
-        case 1: return kernel_for<1, false>(emit);
-        case 2: return vs ? kernel_for<2, true>(emit) : kernel_for<2, false>(emit);
-        case 3: return kernel_for<3, false>(emit);
-        case 4: return vs ? kernel_for<4, true>(emit) : kernel_for<4, false>(emit);
-        case 5: return kernel_for<5, false>(emit);
-        case 6: return vs ? kernel_for<6, true>(emit) : kernel_for<6, false>(emit);
-        case 7: return kernel_for<7, false>(emit);
-        case 8: return vs ? kernel_for<8, true>(emit) : kernel_for<8, false>(emit);
-        case 9: return kernel_for<9, false>(emit);
-        case 10: return vs ? kernel_for<10, true>(emit) : kernel_for<10, false>(emit);
+        case 1: return kernel_for<1, false>(emit, close);
+        case 2: return vs ? kernel_for<2, true>(emit, close) : kernel_for<2, false>(emit, close);
+        case 3: return kernel_for<3, false>(emit, close);
+        case 4: return vs ? kernel_for<4, true>(emit, close) : kernel_for<4, false>(emit, close);
+        case 5: return kernel_for<5, false>(emit, close);
+        case 6: return vs ? kernel_for<6, true>(emit, close) : kernel_for<6, false>(emit, close);
+        case 7: return kernel_for<7, false>(emit, close);
+        case 8: return vs ? kernel_for<8, true>(emit, close) : kernel_for<8, false>(emit, close);
+        case 9: return kernel_for<9, false>(emit, close);
+        case 10: return vs ? kernel_for<10, true>(emit, close) : kernel_for<10, false>(emit, close);
         default: return nullptr;
     }
 }
@@ -954,7 +1306,141 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
 }
 
 // Everything a launch needs that depends only on (plan, depth).
-int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
+// Two-row closure level of a plan below depth-`depth` records (DESIGN.md "Tail
+// closure"): the first search level l >= 1 after which exactly two rows r1 < r2
+// have empty cells, in the same columns and off both diagonals, and the plan
+// covers every empty cell.  Fills the closure fields of prm and returns l, or
+// returns -1 (no closure: a truncated plan, e.g. dls_count_cells; the condition
+// already holds at the records; the 64-bit A/B layout; DLS_CLOSE=0).
+int closure_level(const dls::Plan &plan, int depth, Params *prm) {
+    const int n = plan.n;
+    const bool vs = plan.vs;
+    const int steps = (int)plan.cells.size();
+    const int lay = layout_of(n, vs);
+    if (lay == 2 || n < 3) return -1;
+    if (const char *e = getenv("DLS_CLOSE"))
+        if (atoi(e) == 0) return -1;
+    std::vector<uint8_t> empty(n * n, 1);
+    auto take = [&](int c) {
+        empty[c] = 0;
+        if (vs) empty[(c / n) * n + (n - 1 - c % n)] = 0;
+    };
+    for (int c = 0; c < n * n; ++c)
+        if (plan.pre[c]) empty[c] = 0;
+    for (int s = 0; s < depth; ++s) take(plan.cells[s]);
+    {   // the plan must cover every cell: completions, not partial assignments
+        std::vector<uint8_t> e2 = empty;
+        for (int s = depth; s < steps; ++s) {
+            const int c = plan.cells[s];
+            e2[c] = 0;
+            if (vs) e2[(c / n) * n + (n - 1 - c % n)] = 0;
+        }
+        for (int c = 0; c < n * n; ++c)
+            if (e2[c]) return -1;
+    }
+    for (int l = 0; l <= steps - depth; ++l) {
+        if (l > 0) take(plan.cells[depth + l - 1]);
+        int rows[3], nr = 0;
+        for (int i = 0; i < n && nr < 3; ++i)
+            for (int j = 0; j < n; ++j)
+                if (empty[i * n + j]) { rows[nr++] = i; break; }
+        if (nr != 2) continue;
+        const int r1 = rows[0], r2 = rows[1];
+        bool ok = true;
+        uint32_t open = 0;
+        for (int j = 0; j < n && ok; ++j) {
+            const bool e1 = empty[r1 * n + j], ee2 = empty[r2 * n + j];
+            if (e1 != ee2) ok = false;
+            if (e1 && (r1 == j || r1 + j == n - 1 || r2 == j || r2 + j == n - 1)) ok = false;
+            if (e1 && (!vs || 2 * j < n - 1)) open |= 1u << j;
+        }
+        if (!ok) continue;
+        if (l == 0) return -1;       // already closable at the records: plain search
+        const int h = n / 2, rf = vs ? (h > 0 ? h : 1) : n, rpw32 = 32 / rf, cpw32 = 32 / n;
+        // row r1's word in the mask layout (the closure reads row r1 from it)
+        int rword = 0;
+        switch (lay) {
+            case 0: rword = r1 >= 4; break;
+            case 1: rword = r1 / rpw32; break;
+            case 3: rword = r1 / 3; break;
+            default: rword = r1 == 0 ? 3 : (r1 - 1) / 3;
+        }
+        // walk back over forced cells just before level l (up to 2): the closure
+        // assigns them itself.  A cell qualifies if its row or column has every
+        // other cell assigned before it (one candidate), it lies in neither r1 nor
+        // r2, and (layouts 3, 4) its row shares row r1's word.
+        int nf = 0, fcell[2];
+        {
+            auto assigned_before = [&](int q, int cell) {
+                // assigned a priori, in the records, or at a level < q
+                if (plan.pre[cell]) return true;
+                for (int s2 = 0; s2 < depth + q - 1; ++s2) {
+                    const int c2 = plan.cells[s2];
+                    if (c2 == cell || (vs && (c2 / n) * n + (n - 1 - c2 % n) == cell)) return true;
+                }
+                return false;
+            };
+            // opt-in (DLS_CLOSE_FORCED=1): on DLS8 it trades 2 steps per level-30
+            // node for twice the closure events, and loses (590 -> 703 ms)
+            const char *ef = getenv("DLS_CLOSE_FORCED");
+            const bool walk = ef && atoi(ef) != 0;
+            while (walk && nf < 2 && l - 1 >= 1) {
+                const int cell = plan.cells[depth + l - 1];
+                const int i = cell / n, j = cell % n;
+                if (i == r1 || i == r2) break;
+                if ((lay == 3 || lay == 4) && (lay == 3 ? i / 3 : (i == 0 ? 3 : (i - 1) / 3)) != rword) break;
+                int rowc = 0, colc = 0;
+                for (int k = 0; k < n; ++k) {
+                    if (k != j && assigned_before(l, i * n + k)) ++rowc;
+                    if (k != i && assigned_before(l, k * n + j)) ++colc;
+                }
+                if (vs || (rowc != n - 1 && colc != n - 1)) break;   // (VS: not needed by our plans)
+                fcell[nf++] = cell;
+                --l;
+            }
+        }
+        const int nc = vs ? h : n;                                   // tracked columns
+        const int em = vs ? std::max(h - 1, 1) : std::max(n - 2, 1);  // CloseBase::EM
+        const int E = __builtin_popcount(open);
+        if (E > em || E == nc) return -1;
+        int pad = 0;                                                 // a complete column
+        while (open >> pad & 1u) ++pad;
+        auto sel = [&](int j) -> uint32_t {
+            switch (lay) {
+                case 0: return (uint32_t)j;
+                case 1: return (uint32_t)(32 * (j / cpw32) + (j % cpw32) * n);
+                case 3: return (uint32_t)((j % 3) * n) | (uint32_t)(j / 3) << 5;
+                default: return j == n - 1 ? 3u << 5 : (uint32_t)((j % 3) * n) | (uint32_t)(j / 3) << 5;
+            }
+        };
+        int k = 0;
+        for (int j = 0; j < nc; ++j)
+            if (open >> j & 1u) prm->cl_sel[k++] = sel(j);
+        while (k < 10) prm->cl_sel[k++] = sel(pad);
+        prm->close = 1;
+        prm->cl_open = open;
+        prm->cl_E = E;
+        prm->cl_nf = nf;
+        for (int k = 0; k < nf; ++k) {      // apply in plan order: the earlier cell first
+            Tab t3[3];
+            fill_tab(n, vs, std::vector<int>{fcell[nf - 1 - k]}, t3);
+            prm->cl_fread[k] = t3[1];       // transition 0 reads cell(1)
+            prm->cl_ftog[k] = t3[2];        // transition 1 toggles cell(1)
+        }
+        switch (lay) {
+            case 0: prm->cl_rword = r1 >= 4; prm->cl_rshift = 8 * (r1 & 3); break;
+            case 1: prm->cl_rword = r1 / rpw32; prm->cl_rshift = (r1 % rpw32) * rf; break;
+            case 3: prm->cl_rword = r1 / 3; prm->cl_rshift = n * (r1 % 3); break;
+            default:
+                if (r1 == 0) { prm->cl_rword = 3; prm->cl_rshift = n; }
+                else { prm->cl_rword = (r1 - 1) / 3; prm->cl_rshift = n * ((r1 - 1) % 3); }
+        }
+        return l;
+    }
+    return -1;
+}
+
+int prepare_plan(const dls::Plan &plan, int depth, Params *prm, bool allow_close = true) {
     const int n = plan.n;
     const bool symmetric = plan.vs;
     const int steps = (int)plan.cells.size();
@@ -974,7 +1460,11 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     }
     std::memset(prm, 0, sizeof(*prm));
     prm->L = steps - depth;
-    std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.end());
+    if (allow_close) {
+        const int lc = closure_level(plan, depth, prm);
+        if (lc >= 0) prm->L = lc;
+    }
+    std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.begin() + depth + prm->L);
     fill_tab(n, symmetric, level_cells, prm->tab);
     for (size_t l = 0; l < level_cells.size(); ++l) prm->level_cell[l + 1] = (uint8_t)level_cells[l];
     // assigned-cell pattern of a depth-`depth` prefix
@@ -993,22 +1483,29 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm) {
     return DLS_OK;
 }
 
-int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm) {
+int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm, bool allow_close = true) {
     dls::Plan plan;
     if (!dls::make_plan(n, symmetric, fixed_first_row, &plan)) {
         dls::set_error("dls_count: unsupported (n, symmetric, fixed_first_row)");
         return DLS_E_ARG;
     }
-    return prepare_plan(plan, depth, prm);
+    return prepare_plan(plan, depth, prm, allow_close);
 }
 
-size_t smem_bytes(int n, bool vs, int L, int nthreads) {
-    const size_t sw = layout_of(n, vs) >= 2 ? 2 : 4;
-    return (size_t)(L + 2) * 32 * 32 + (size_t)(L + 2) * nthreads * sw;
+size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close) {
+    const int lay = layout_of(n, vs);
+    const size_t sw = lay == 0 ? 1 : 2;                       // Layout::SW
+    const size_t stack = (size_t)(L + 1 + 4 / sw) * nthreads * sw;
+    const size_t base = (size_t)(L + 2) * 32 * 32 + ((stack + 15) & ~(size_t)15);
+    if (!close) return base;
+    const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
+    const size_t cq = lay == 0 ? 9 : (lay == 1 ? 7 : 6);     // Layout::CQ
+    return base + cq * nthreads * ew * 4 + (size_t)nthreads * 4;   // queues + counters
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
-    KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr);
+    const bool close = prm.close && prm.emit == nullptr;
+    KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr, close);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
     cudaError_t e;
     int dev = 0, sms = 0, smem_max = 0;
@@ -1021,8 +1518,9 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     const int lay = layout_of(n, vs);
     int nthreads = 1024;                   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
-    while (lay >= 2 && nthreads > 32 && smem_bytes(n, vs, prm.L, nthreads) > (size_t)smem_max) nthreads -= 32;
-    const size_t smem = smem_bytes(n, vs, prm.L, nthreads);
+    // (a multiple of 64, so that the u16 stack's lanes keep distinct banks)
+    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, close) > (size_t)smem_max) nthreads -= 64;
+    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, close);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute");
@@ -1199,7 +1697,7 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
     int64_t extra_nodes = 0;
     bool bad_prefix = false;
     if (refine_below < 0) refine_below = kRefineTarget / 8;
-    if (n_prefix > 0 && n_prefix < refine_below && depth + 1 <= steps - kMinSearchLevels) {
+    if (n_prefix > 0 && n_prefix < refine_below && depth + 1 <= steps - kMinSearchLevels && prm.L > 1) {
         if (in_dev) {
             h_in.resize((size_t)n_prefix * nn);
             if ((e = cudaMemcpyAsync(h_in.data(), prefix_buf, h_in.size(), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
@@ -1211,7 +1709,9 @@ int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_
             if (!dls::valid_record(plan, depth, src + p * nn)) bad_prefix = true;
         int d1 = depth;
         int64_t cnt = n_prefix;
-        while (cnt < kRefineTarget && d1 + 1 <= steps - kMinSearchLevels) {
+        // stay above the closure level (records at it could not use the closure)
+        const int close_pos = depth + prm.L;
+        while (cnt < kRefineTarget && d1 + 1 <= steps - kMinSearchLevels && d1 + 1 < close_pos) {
             ++d1;
             cnt = dls::refine(plan, depth, d1, src, n_prefix, nullptr, nullptr, 0, nullptr);
         }
@@ -1301,6 +1801,15 @@ extern "C" int dls_count(int n, int symmetric, int fixed_first_row, int depth,
     return dls::count_records(plan, depth, prefix_buf, n_prefix, out_counts, out_total, out_nodes, stream);
 }
 
+extern "C" int dls_search_levels(int n, int symmetric, int fixed_first_row, int depth, int32_t *out_levels) {
+    if (!out_levels) { dls::set_error("dls_search_levels: null output"); return DLS_E_ARG; }
+    Params prm;
+    const int rc = prepare(n, symmetric, fixed_first_row, depth, &prm);
+    if (rc) return rc;
+    *out_levels = prm.L;
+    return DLS_OK;
+}
+
 extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth, const uint8_t *d_prefixes,
                             int64_t n_prefix, uint8_t *d_out, int64_t capacity, void *stream) {
     int rc = have_device();
@@ -1311,7 +1820,7 @@ extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth
         return DLS_E_ARG;
     }
     Params prm;
-    if ((rc = prepare(n, symmetric, fixed_first_row, depth, &prm))) return rc;
+    if ((rc = prepare(n, symmetric, fixed_first_row, depth, &prm, false))) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     u64 *d_stats = nullptr;
     cudaError_t e = cudaMallocAsync((void **)&d_stats, DLS_STATS_WORDS * sizeof(u64), s);

@@ -25,12 +25,32 @@ pytestmark = pytest.mark.gpu
 
 
 def _oracle_per_prefix(n, vs, recs, depth, fixed=True):
+    """Oracle counts of every record, and the oracle's node total of the search
+    the GPU runs: the plan cells below the records down to the level
+    dls_search_levels reports (the two-row closure level, R15)."""
     pre = np.zeros((n, n), np.int32)
     if fixed:
         pre[0, :] = 1
     order = oracle.plan(n, vs, pre)[depth:]
-    out = [oracle.count(n, vs, synth.to_int_grid(r), order) for r in recs]
-    return np.array([c for c, _ in out], dtype=np.uint64), sum(nd for _, nd in out)
+    levels = D.dls_search_levels(n, depth, vs, fixed) if len(order) else 0
+    out = [oracle.count_levels(n, vs, synth.to_int_grid(r), order) for r in recs]
+    return np.array([c for c, _ in out], dtype=np.uint64), sum(sum(lv[:levels]) for _, lv in out)
+
+
+class closure_off:
+    """DLS_CLOSE=0 for the calls inside: the plain search over every level (its
+    node count is the oracle's full-tree count)."""
+    def __enter__(self):
+        import os
+        self.old = os.environ.get("DLS_CLOSE")
+        os.environ["DLS_CLOSE"] = "0"
+
+    def __exit__(self, *a):
+        import os
+        if self.old is None:
+            os.environ.pop("DLS_CLOSE", None)
+        else:
+            os.environ["DLS_CLOSE"] = self.old
 
 
 def _gpu(n, vs, recs, depth, fixed=True):
@@ -120,11 +140,15 @@ def test_config4_vs10_seeded_prefixes():
     gold = _read_golden("vs10_prefix_counts.txt")
     for i, (c, _) in gold.items():
         assert int(counts[i]) == c, i
-    # the golden prefixes alone: same counts, and the search visits exactly the
-    # oracle's nodes (full-size workunits, refined to ~1.2M records on the host)
+    # the golden prefixes alone: same counts, and the plain search (closure off)
+    # visits exactly the oracle's full-tree nodes (full-size workunits, refined
+    # to ~1.2M records on the host)
     idx = sorted(gold)
-    c2, t2, nodes = _gpu(n, vs, recs[idx], d)
+    c2, t2, _ = _gpu(n, vs, recs[idx], d)
     assert [int(x) for x in c2] == [gold[i][0] for i in idx]
+    with closure_off():
+        c3, t3, nodes = _gpu(n, vs, recs[idx], d)
+    assert [int(x) for x in c3] == [gold[i][0] for i in idx]
     assert nodes == sum(gold[i][1] for i in idx)
 
 
@@ -158,8 +182,11 @@ def test_config5_dls9_seeded_prefixes():
     for i, (c, _) in gold.items():
         assert int(counts[i]) == c, i
     idx = sorted(gold)
-    c2, t2, nodes = _gpu(n, False, recs[idx], d)
+    c2, t2, _ = _gpu(n, False, recs[idx], d)
     assert [int(x) for x in c2] == [gold[i][0] for i in idx]
+    with closure_off():
+        c3, t3, nodes = _gpu(n, False, recs[idx], d)
+    assert [int(x) for x in c3] == [gold[i][0] for i in idx]
     assert nodes == sum(gold[i][1] for i in idx)
 
 
@@ -374,3 +401,42 @@ def test_monte_carlo_estimate_small_order():
     exact = oracle.count_all(7)
     assert abs(r["knuth"] - exact) < 4 * r["knuth_se"]
     assert r["N_k"] == oracle.count_prefixes(7, False, oracle.first_row_grid(7), list(range(7, 14)), 7)
+
+
+# ------------------------------------------------------------------ two-row closure
+
+@pytest.mark.parametrize("n,vs,fixed", [(5, False, True), (6, False, False), (7, False, True), (4, True, True),
+                                        (6, True, True), (8, True, True), (6, True, False)])
+def test_closure_equals_plain_search(n, vs, fixed):
+    """The closure kernel and the plain search (DLS_CLOSE=0) give the same
+    per-prefix counts; each one's nodes are the oracle's nodes of the levels it
+    searches (truncated tree / full tree)."""
+    d = D.default_split_depth(n, vs, fixed)
+    recs = D.dls_split(n, d, vs, fixed)
+    want, want_nodes = _oracle_per_prefix(n, vs, recs, d, fixed)
+    c1, t1, nd1 = _gpu(n, vs, recs, d, fixed)
+    with closure_off():
+        c0, t0, nd0 = _gpu(n, vs, recs, d, fixed)
+        levels_full = D.dls_search_levels(n, d, vs, fixed)
+    assert (c1 == want).all() and (c0 == want).all()
+    assert nd1 == want_nodes
+    pre = np.zeros((n, n), np.int32)
+    if fixed:
+        pre[0, :] = 1
+    order = oracle.plan(n, vs, pre)[d:]
+    assert levels_full == len(order)
+    full = sum(oracle.count(n, vs, synth.to_int_grid(r), order)[1] for r in recs)
+    assert nd0 == full and nd1 <= full
+
+
+def test_closure_dls8_sample_and_nodes():
+    """DLS8 workunits: closure counts = oracle counts; nodes = the oracle's nodes
+    of levels 1..30 (the plan's rows 3/4 tail, 12 cells, is closed in form)."""
+    n, d = 8, D.default_split_depth(8)
+    assert D.dls_search_levels(n, d) == 30 and len(D.dls_plan(n)[0]) - d == 42
+    recs = D.dls_split(n, d)
+    rng = np.random.default_rng(30)
+    recs = recs[rng.choice(len(recs), 40, replace=False)]
+    counts, _, nodes = _gpu(n, False, recs, d)
+    want, want_nodes = _oracle_per_prefix(n, False, recs, d)
+    assert (counts == want).all() and nodes == want_nodes

@@ -207,3 +207,18 @@ def test_hourglass_count_order8():
     last = [(n - 1) * n + j for j in range(n) if (n - 1) * n + j not in diag]
     assert oracle.count_prefixes(n, False, g, diag + last, len(diag) + len(last)) == \
         paper_counts()["hourglass8"]
+
+
+@pytest.mark.parametrize("n,vs,fixed", [(4, False, True), (5, False, False), (6, False, True), (6, True, True),
+                                        (7, False, True)])
+def test_count_levels_pins(n, vs, fixed):
+    """oracle.count_levels: entry k = consistent assignments of the first k+1
+    cells (= count_prefixes, an independent enumeration), the entries add up to
+    count()'s nodes, and the last one is the number of completions."""
+    g = oracle.first_row_grid(n) if fixed else oracle.empty_grid(n)
+    order = oracle.plan_for_grid(n, vs, g)
+    c, lv = oracle.count_levels(n, vs, g, order)
+    cc, nodes = oracle.count(n, vs, g, order)
+    assert c == cc and sum(lv) == nodes and lv[-1] == c
+    for k in range(0, len(order), max(1, len(order) // 9)):
+        assert lv[k] == oracle.count_prefixes(n, vs, g, order, k + 1)
