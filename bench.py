@@ -6,7 +6,8 @@ fixed (BASELINE.json config 3; 7 447 587 840 squares), on B200s.
 
 A step is one pass of the hot path over the whole workload: every one of the
 547 896 depth-14 workunits (first row + both diagonals, P:481 / Fig. 1 order)
-searched to the leaves by the sm_100a kernel.
+searched by the sm_100a kernel down to the two-row level (the last two open
+rows are counted in closed form).
 
 value  : squares/s with the workunits resident in HBM; per-step CUDA events on
          the launch stream, L2 flushed (256 MiB write) before every step, max
@@ -41,13 +42,21 @@ SYMMETRIC = False
 WORKLOAD = "dls8_first_row_fixed_full"
 METRIC = "diagonal Latin squares enumerated/sec"
 UNIT = "squares/s"
-NCU_JSON = "r1_ncu_b256.json"   # the committed ncu --set full capture of the timed kernel
+NCU_JSON = "r2_ncu_close.json"  # the committed ncu --set full capture of the timed kernel
+                                 # (used only if its count_cu_sha matches the source)
 # Algorithmic integer operations per search node: one pass
 # of Alg. 4's loop body for a non-diagonal cell:
 #   CR = Rows|Columns (1), L = AllN^CR (1), L != 0 test (1), b = L&-L (2),
 #   mark Rows/Columns (2), unmark Rows/Columns (2), L &= L-1 (2), loop exit test
 #   amortised (1)  -> 12
 OPS_PER_NODE = 12
+# Algorithmic integer operations per two-row closure,
+# |J| = 6 open columns for the N=8 plan: per column complement (1), isolate the
+# low value (2), fold it into t (1) -> 24; GF(2) elimination: per pivot isolate
+# (2) + rank (1) + t update (2) -> 30, per pair of columns test + xor (2) x 15 ->
+# 30; final test and shift (3) -> 87
+OPS_PER_CLOSURE = 87
+DLS8_COUNT = 7447587840
 PAPER_CONTEXT = "paper: 5.8e6 DLS8 squares/s on one core of an Intel Core i7-6770 (Table 1, P:281); context only"
 
 
@@ -121,17 +130,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def oracle_workunits():
+    """The workunits of the config from the ORACLE alone (its plan and prefix
+    enumeration): every consistent assignment of the first `depth` plan
+    cells, depth = the first prefix length covering both diagonals (Fig. 1)."""
+    import oracle
+    plan = oracle.plan(N_ORDER)
+    diag = {i * N_ORDER + j for i in range(1, N_ORDER) for j in (i, N_ORDER - 1 - i)}
+    depth = next(k for k in range(len(plan) + 1) if diag <= set(plan[:k]))
+    recs = oracle.prefixes(N_ORDER, SYMMETRIC, oracle.first_row_grid(N_ORDER), plan, depth)
+    return plan, depth, recs
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle on bounded samples of the workunits."""
+    """--impl reference: the CPU oracle on bounded samples of the workunits
+    (loads only oracle/; no product code)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    import synth
-    from paper_1709_02599_b200 import _binding as B  # host-side split only (no GPU)
-    plan = oracle.plan(N_ORDER)
-    depth = B.dls_plan(N_ORDER)[2]
-    recs = B.dls_split(N_ORDER, depth)
+    plan, depth, recs = oracle_workunits()
     order = plan[depth:]
     rng = np.random.default_rng(20260)
     budget = float(os.environ.get("DLS_REF_STEP_SECONDS", "4"))
@@ -141,7 +159,7 @@ def run_reference(args):
         s_sq = s_nd = 0
         while time.perf_counter() - t0 < budget:
             r = recs[int(rng.integers(len(recs)))]
-            c, nd = oracle.count(N_ORDER, SYMMETRIC, synth.to_int_grid(r), order)
+            c, nd = oracle.count(N_ORDER, SYMMETRIC, r, order)
             s_sq += c
             s_nd += nd
             if step >= args.warmup:
@@ -178,16 +196,17 @@ def pick_depth(world: int, lanes_per_gpu: int = 148 * 1024) -> int:
     return d
 
 
-def cpu_baseline(recs, depth, seconds: float):
+def cpu_baseline(seconds: float):
+    """The oracle, as it stands, on random workunits it enumerates itself."""
     import oracle
-    import synth
-    order = oracle.plan(N_ORDER)[depth:]
+    plan, depth, recs = oracle_workunits()
+    order = plan[depth:]
     rng = np.random.default_rng(1709)
     t0 = time.perf_counter()
     sq = nd = k = 0
     while time.perf_counter() - t0 < seconds:
         r = recs[int(rng.integers(len(recs)))]
-        c, n_ = oracle.count(N_ORDER, SYMMETRIC, synth.to_int_grid(r), order)
+        c, n_ = oracle.count(N_ORDER, SYMMETRIC, r, order)
         sq += c
         nd += n_
         k += 1
@@ -251,7 +270,7 @@ def main():
 
     # ---- timed: K steps, per-step events on the launch stream, L2 flushed in between
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    counts, nodes_l = [], []
+    counts, nodes_l, events_l = [], [], []
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
@@ -264,6 +283,7 @@ def main():
             st = d_stats.cpu()
             counts.append(reduce_count(int(st[0])))
             nodes_l.append(reduce_count(int(st[1])))
+            events_l.append(reduce_count(int(st[8])))
             assert int(st[2]) == 0
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -273,8 +293,9 @@ def main():
     total_ms = allreduce_max(local_ms, device=dev)
     clocks = clk.summary()
     squares = counts[0]
-    if squares != 7447587840:
-        raise SystemExit("wrong count %d" % squares)
+    # every timed step must reproduce P:476 and visit the same tree
+    if any(c != DLS8_COUNT for c in counts) or len(set(nodes_l)) != 1 or len(set(events_l)) != 1:
+        raise SystemExit("timed steps disagree: counts %s nodes %s closures %s" % (counts, nodes_l, events_l))
     value = squares * args.steps / (total_ms / 1e3)
     nodes_per_sec = nodes_l[0] * args.steps / (total_ms / 1e3)
 
@@ -303,10 +324,10 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            assert e2e_step() == 7447587840
+            assert e2e_step() == DLS8_COUNT
         torch.cuda.synchronize()
         el = allreduce_max(time.perf_counter() - t0, device=dev)
-        e2e = {"value": 7447587840 * e2e_steps / el, "unit": UNIT,
+        e2e = {"value": DLS8_COUNT * e2e_steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(pin_mine.numel()), "d2h_bytes_per_step": 8 * B.DLS_STATS_WORDS,
                "includes": "host dls_split into pinned memory + H2D of the workunits + search + D2H of the count"}
 
@@ -315,13 +336,21 @@ def main():
         sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
         peak = int_issue_peak_tops(sm_mhz)
         per_launch_ms = local_ms / args.steps
-        achieved = nodes_l[0] / world * OPS_PER_NODE / (per_launch_ms / 1e3) / 1e12
-        ncu = {}
+        ops = nodes_l[0] * OPS_PER_NODE + events_l[0] * OPS_PER_CLOSURE
+        achieved = ops / world / (per_launch_ms / 1e3) / 1e12
+        ncu, ncu_note = {}, ""
         try:
+            import hashlib
             with open(os.path.join(ROOT, "profiles", NCU_JSON)) as f:
                 ncu = json.load(f)
+            src = os.path.join(ROOT, "paper_1709_02599_b200", "csrc", "count.cu")
+            sha = hashlib.sha256(open(src, "rb").read()).hexdigest()[:16]
+            if ncu.get("count_cu_sha") != sha:
+                ncu_note = "capture %s is of another count.cu (%s != %s): ncu fields omitted" % (
+                    NCU_JSON, ncu.get("count_cu_sha"), sha)
+                ncu = {}
         except (OSError, ValueError):
-            pass
+            ncu, ncu_note = {}, "no capture %s" % NCU_JSON
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -329,22 +358,25 @@ def main():
             "config": {"workload": WORKLOAD, "n": N_ORDER, "symmetric": SYMMETRIC, "first_row_fixed": True,
                        "prefix_depth": depth, "n_prefix": int(recs_all.shape[0]),
                        "squares_per_step": squares, "nodes_per_step": nodes_l[0],
+                       "closures_per_step": events_l[0], "search_levels": B.dls_search_levels(N_ORDER, depth),
                        "l2": "flushed before every step (256 MiB device write)",
                        "parallelism": "workunits round-robin over %d rank(s)" % world},
             "nodes_per_sec": nodes_per_sec,
+            "closures_per_sec": events_l[0] * args.steps / (total_ms / 1e3),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                          "frac": achieved / peak,
                          "traffic": (ncu["dram_read_bytes"] + ncu["dram_write_bytes"]) if ncu else None,
-                         "traffic_note": "DRAM bytes per launch from the committed ncu --set full capture "
-                                         "(profiles/%s) = the 35 MB of workunit records: the "
-                                         "search itself never touches HBM" % NCU_JSON,
+                         "traffic_note": ncu_note or ("DRAM bytes per launch from the committed ncu --set full "
+                                                      "capture (profiles/%s) = the 35 MB of workunit records: "
+                                                      "the search itself never touches HBM" % NCU_JSON),
+                         "ops_per_node": OPS_PER_NODE, "ops_per_closure": OPS_PER_CLOSURE,
                          "issue_slots_busy_ncu": (ncu.get("issue_slots_busy_pct", 0) / 100.0) if ncu else None,
                          # the unit that binds the kernel: the shared-memory data pipe
                          # (table + stack loads), not the integer issue rate
                          "smem_pipe_busy_ncu": (ncu.get("smem_lsu_wavefronts_pct", 0) / 100.0) if ncu else None,
                          "note": "integer-issue roofline at %.0f MHz (MEASURED_PEAKS sm_max_mhz): 148 SMs x 4 SMSP x "
-                                 "32 lanes; achieved = %d algorithmic int ops/node (Alg. 4) x nodes / kernel time"
-                                 % (sm_mhz, OPS_PER_NODE)},
+                                 "32 lanes; achieved = (%d int ops x nodes the kernel visits (Alg. 4 loop body) + "
+                                 "%d x two-row closures) / kernel time" % (sm_mhz, OPS_PER_NODE, OPS_PER_CLOSURE)},
             "clocks": clocks,
             "gpu_launches": args.steps * B.dls_kernel_launches(),
             "wall_ms_timed_region": t_wall * 1e3,
@@ -353,7 +385,7 @@ def main():
         if e2e:
             line["e2e"] = e2e
         if world == 1 and args.cpu_seconds > 0:
-            line["cpu_baseline"] = cpu_baseline(recs_all, depth, args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -35,9 +35,10 @@
  * writes nothing it did not document as written.  No call aborts the process.
  * Thread safety: calls are reentrant; dls_count serialises on its own stream.
  * Device memory: per-launch scratch (the 2 MB donation pool, the symmetry-breaking
- * buffers) comes from the device's default stream-ordered memory pool; on first
- * use the library sets that pool's release threshold to 1 GB so freed scratch
- * stays cached between calls (DLS_POOL_KEEP=0 in the environment skips this).
+ * buffers) comes from the library's own stream-ordered memory pool (one per
+ * device, created on first use; freed scratch stays cached up to 1 GB,
+ * DLS_POOL_KEEP=<bytes> in the environment changes that; dls_count_sb trims it
+ * back to 64 MB on return).  The process's default pool is not touched.
  */
 #ifndef DLS_B200_H
 #define DLS_B200_H
@@ -165,10 +166,11 @@ int dls_search_levels(int n, int symmetric, int fixed_first_row, int depth, int3
  *                  them; dls_count then returns DLS_E_CUDA), [3] work-queue
  *                  cursor, [4] subtree donations, [5] busy lane-bursts,
  *                  [6] lane-bursts (lane utilisation = [5]/[6]), [7] subtrees
- *                  published to the device-wide donation pool.
+ *                  published to the device-wide donation pool, [8] two-row
+ *                  states counted in closed form (dls_search_levels), [9] 0.
  * Returns DLS_OK or DLS_E_ARG/DLS_E_CUDA/DLS_E_NODEVICE for launch-time errors.
  */
-#define DLS_STATS_WORDS 8
+#define DLS_STATS_WORDS 10
 int dls_count_async(int n, int symmetric, int fixed_first_row, int depth,
                     const uint8_t *d_prefixes, int64_t n_prefix,
                     uint64_t *d_counts, uint64_t *d_stats, void *stream);

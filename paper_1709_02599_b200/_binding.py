@@ -16,7 +16,7 @@ from . import build as _build
 
 DLS_EMPTY = 0xFF
 DLS_MAX_ORDER = 10
-DLS_STATS_WORDS = 8
+DLS_STATS_WORDS = 10
 DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
@@ -142,6 +142,34 @@ def _ptr(a) -> Tuple[int, object]:
     raise TypeError("expected numpy array or torch tensor")
 
 
+def _dtype_name(a) -> str:
+    return str(a.dtype).replace("torch.", "")
+
+
+def _check_records(a, n: int, what: str) -> int:
+    """Records must be uint8 of shape (k, n, n) (or (k, n*n)); returns k."""
+    if a is None:
+        return 0
+    if _dtype_name(a) != "uint8":
+        raise ValueError("%s: records must be uint8, got %s" % (what, _dtype_name(a)))
+    shape = tuple(a.shape)
+    if not (len(shape) == 3 and shape[1:] == (n, n)) and not (len(shape) == 2 and shape[1] == n * n):
+        raise ValueError("%s: records must have shape (k, %d, %d), got %s" % (what, n, n, shape))
+    return int(shape[0])
+
+
+def _check_counts(c, k: int, what: str, device=None):
+    """Per-prefix counts must be 8-byte integers with room for k entries."""
+    if c is None:
+        return
+    if _dtype_name(c) not in ("uint64", "int64"):
+        raise ValueError("%s: counts must be uint64/int64, got %s" % (what, _dtype_name(c)))
+    if int(np.prod(tuple(c.shape))) < k:
+        raise ValueError("%s: counts hold %d entries, need %d" % (what, int(np.prod(tuple(c.shape))), k))
+    if device is not None and hasattr(c, "device") and str(c.device) != str(device):
+        raise ValueError("%s: counts on %s but records on %s" % (what, c.device, device))
+
+
 def dls_count(n: int, depth: int, prefixes, symmetric: bool = False, fixed_first_row: bool = True,
               out_counts=None, stream: Optional[int] = None) -> Tuple[int, int]:
     """Count completions of every prefix on the GPU -> (total, nodes).
@@ -150,7 +178,8 @@ def dls_count(n: int, depth: int, prefixes, symmetric: bool = False, fixed_first
     ``out_counts``: optional uint64 numpy array / int64 torch tensor of length count.
     ``stream``: cudaStream_t handle (e.g. ``torch.cuda.current_stream().cuda_stream``).
     """
-    n_prefix = int(prefixes.shape[0]) if prefixes is not None else 0
+    n_prefix = _check_records(prefixes, n, "dls_count")
+    _check_counts(out_counts, n_prefix, "dls_count")
     pp, keep1 = _ptr(prefixes)
     cp, keep2 = _ptr(out_counts)
     tot = ctypes.c_uint64(0)
@@ -164,6 +193,10 @@ def dls_count(n: int, depth: int, prefixes, symmetric: bool = False, fixed_first
 def dls_count_async(n: int, depth: int, d_prefixes, d_counts, d_stats, symmetric: bool = False,
                     fixed_first_row: bool = True, stream: Optional[int] = None) -> None:
     """Enqueue the search on ``stream``; all tensors must be CUDA tensors."""
+    k = _check_records(d_prefixes, n, "dls_count_async")
+    _check_counts(d_counts, k, "dls_count_async", getattr(d_prefixes, "device", None))
+    if d_stats is None or _dtype_name(d_stats) not in ("uint64", "int64") or int(np.prod(tuple(d_stats.shape))) < DLS_STATS_WORDS:
+        raise ValueError("dls_count_async: stats must be %d uint64/int64 words" % DLS_STATS_WORDS)
     pp, k1 = _ptr(d_prefixes)
     cp, k2 = _ptr(d_counts)
     sp, k3 = _ptr(d_stats)
@@ -203,6 +236,9 @@ def dls_emit(n: int, depth: int, d_prefixes, d_out, symmetric: bool = False, fix
              stream: Optional[int] = None) -> int:
     """Write every completion of the (CUDA) records into d_out (CUDA uint8, (cap, n, n));
     returns the number of completions."""
+    k = _check_records(d_prefixes, n, "dls_emit")
+    if d_out is not None:
+        _check_records(d_out, n, "dls_emit (output)")
     pp, k1 = _ptr(d_prefixes)
     op, k2 = _ptr(d_out)
     cap = int(d_out.shape[0]) if d_out is not None else 0

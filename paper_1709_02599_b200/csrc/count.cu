@@ -98,6 +98,7 @@ enum CheckBits {
 // [5] slots released (read completely; producers bound tail - released so a
 //     claimed slot is never overwritten before its reader is done),
 // then kPoolSlots slots of kSlotWords: w0 = ticket+1 once written, w1 = pid,
+// w2 = ticket+1 once read (a producer of the next lap waits for it),
 // w3 = split level | untried siblings << 16, w4.. = the values (bit indices) of
 // levels 1..split-1, 4 bits each.
 constexpr uint32_t kPoolSlots = 16384;
@@ -805,9 +806,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // [0] squares, [1] nodes, [2] donations, [3] busy lane-bursts,
     // [4] lane-bursts -- keeps them out of the registers of the search loop
     // [5] (lane 0 only): ns between pool polls of this warp while idle
-    __shared__ u64 wacc[32][6];
+    // [6] closure events evaluated
+    __shared__ u64 wacc[32][7];
     u64 *const acc = wacc[tid >> 5];
-    if (lane < 6) acc[lane] = 0;
+    if (lane < 7) acc[lane] = 0;
     __syncwarp();
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
@@ -849,6 +851,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         cq_r += max(0, min(32 - pex, c));
         if (cq_r == cq_n) { cq_r = cq_n = 0; cq_w = cq_lane0; }
         cq_rot = (cq_rot + 7u) & 31u;
+        if (lane == 0) acc[6] += (u64)min(total, 32);
         return total;
     };
     auto close_drain = [&]() {
@@ -962,6 +965,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
                               kChkPoolGet);
                     for (int l = 1; l < split; ++l)
                         S[(l + 1) * NT] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
+                    // consumed: the producer of ticket + kPoolSlots may reuse the slot
+                    __threadfence();
+                    *const_cast<volatile uint32_t *>(slot + 2) = ticket + 1u;
                     adopt = true;
                 }
                 __syncwarp();
@@ -1039,6 +1045,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
                             DLS_CHECK(ticket - ld_acquire(pool + 5) < kPoolSlots && 4 + (dsplit + 6) / 8 <= kSlotWords,
                                       kChkPoolPut);
                             uint32_t *slot = pool + kPoolHeader + (ticket % kPoolSlots) * kSlotWords;
+                            // wait until the slot's previous occupant (ticket - kPoolSlots)
+                            // has been read completely (its reader stamps w2)
+                            const uint32_t prev = ticket >= kPoolSlots ? ticket + 1u - kPoolSlots : 0u;
+                            while (ld_acquire(slot + 2) != prev) __nanosleep(32);
                             slot[1] = (uint32_t)pid;
                             slot[3] = (uint32_t)dsplit | (drest << 16);
                             for (int w = 0; w < (dsplit + 6) / 8; ++w) {
@@ -1187,14 +1197,15 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // ------------------------------------------------ block reduction, 1 atomic per block
     __syncthreads();
     if (tid == 0) {
-        u64 a[5] = {0, 0, 0, 0, 0};
+        u64 a[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int w = 0; w < NT / 32; ++w)
-            for (int k = 0; k < 5; ++k) a[k] += wacc[w][k];
+            for (int k = 0; k < 7; ++k) a[k] += wacc[w][k];
         atomicAdd(p.stats + 0, a[0]);   // squares
         atomicAdd(p.stats + 1, a[1]);   // nodes (assignments, leaves included)
         atomicAdd(p.stats + 4, a[2]);   // donations
         atomicAdd(p.stats + 5, a[3]);   // busy lane-bursts
         atomicAdd(p.stats + 6, a[4]);   // lane-bursts
+        atomicAdd(p.stats + 8, a[6]);   // closure events
         if (!EMIT) atomicMax(p.stats + 7, (u64)ld_acquire(pool + 3));   // subtrees published to the pool
         stamp_first(pool, kStampFirstExit);
         atomicMax(reinterpret_cast<u64 *>(pool + kStampLastExit), globaltimer());
@@ -1514,7 +1525,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
         return cuda_fail(e, "cudaDeviceGetAttribute");
     if ((e = cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
         return cuda_fail(e, "cudaDeviceGetAttribute");
-    smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators)
+    smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators, 1.75 KB)
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     const int lay = layout_of(n, vs);
     int nthreads = 1024;                   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
@@ -1527,14 +1538,18 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     // one CTA per SM even for few workunits: warps without a workunit start by
     // taking donated subtrees from the device-wide pool
     void *pool = nullptr;
-    dls::keep_pool_memory(dev);
-    if ((e = cudaMallocAsync(&pool, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(pool)");
+    if ((e = dls::scratch_alloc(&pool, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "scratch_alloc(pool)");
     if ((e = cudaMemsetAsync(pool, 0, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(pool)");
     Params q = prm;
     q.pool = (uint32_t *)pool;
     q.total_warps = (uint32_t)sms * (uint32_t)(nthreads / 32);
-    fn<<<(unsigned)sms, nthreads, smem, stream>>>(q);
-    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "kernel launch");
+    // Cooperative launch: the exit test waits for every warp of the grid to have
+    // registered, so all CTAs must be resident at once; the launch guarantees it
+    // or fails (e.g. while other work holds SMs) instead of hanging.
+    void *args[] = {&q};
+    if ((e = cudaLaunchCooperativeKernel((const void *)fn, dim3((unsigned)sms), dim3((unsigned)nthreads), args, smem,
+                                         stream)) != cudaSuccess)
+        return cuda_fail(e, "kernel launch (cooperative)");
     if (getenv("DLS_TIMING")) {   // end-game timeline of this launch (synchronises)
         u64 st[8];
         cudaMemcpyAsync(st, (uint32_t *)pool + kStampStart, sizeof(st), cudaMemcpyDeviceToHost, stream);
@@ -1641,22 +1656,55 @@ int error_word(u64 w, const char *who) {
 
 namespace dls {
 
-// The donation pool comes from the device's default stream-ordered memory pool.
-// With its default release threshold (0) every synchronisation hands the freed
-// 2 MB back to the OS, and now and then that costs 0.25-1.2 s after the kernel
-// has finished (profiles/r1_e2e_variance.log).  Keep up to 1 GB cached instead
-// (the symmetry-breaking driver's scratch comes from the same pool; once per
-// device; DLS_POOL_KEEP=0 restores the default for A/B).
-void keep_pool_memory(int dev) {
-    static std::once_flag once[64];
-    std::call_once(once[dev & 63], [dev]() {
-        const char *e = getenv("DLS_POOL_KEEP");
-        if (e && atoi(e) == 0) return;
-        cudaMemPool_t mp;
-        if (cudaDeviceGetDefaultMemPool(&mp, dev) != cudaSuccess) { cudaGetLastError(); return; }
-        uint64_t keep = 1ull << 30;
-        if (cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) cudaGetLastError();
+// Scratch device memory (the donation pool, the symmetry-breaking buffers) comes
+// from the library's own stream-ordered memory pool, one per device, created on
+// first use.  Its release threshold is 1 GB: with the default threshold (0)
+// every synchronisation hands the freed memory back to the OS, and that used to
+// cost 0.25-1.2 s after the kernel had finished (profiles/r1_e2e_variance.log).
+// The process's default pool (PyTorch's cudaMallocAsync backend, other users)
+// is left alone.
+namespace {
+std::once_flag g_pool_once[64];
+cudaMemPool_t g_pools[64];
+cudaError_t g_pool_status[64];
+
+// this device's pool (created on first use), or the creation error
+cudaError_t library_pool(cudaMemPool_t *out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::call_once(g_pool_once[dev & 63], [dev]() {
+        cudaMemPoolProps props;
+        std::memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaError_t e1 = cudaMemPoolCreate(&g_pools[dev & 63], &props);
+        if (e1 == cudaSuccess) {
+            uint64_t keep = 1ull << 30;
+            if (const char *k = getenv("DLS_POOL_KEEP")) keep = (uint64_t)atoll(k);
+            e1 = cudaMemPoolSetAttribute(g_pools[dev & 63], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        g_pool_status[dev & 63] = e1;
     });
+    *out = g_pools[dev & 63];
+    return g_pool_status[dev & 63];
+}
+}  // namespace
+
+cudaError_t scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream) {
+    cudaMemPool_t mp;
+    const cudaError_t e = library_pool(&mp);
+    if (e != cudaSuccess) return e;
+    return cudaMallocFromPoolAsync(ptr, bytes, mp, stream);
+}
+
+// Hand cached scratch above keep_bytes back (after large symmetry-breaking calls).
+void scratch_trim(size_t keep_bytes) {
+    cudaMemPool_t mp;
+    if (library_pool(&mp) == cudaSuccess) cudaMemPoolTrimTo(mp, keep_bytes);
+    cudaGetLastError();
 }
 
 // dls_count for an arbitrary plan (the standard one, or the hourglass plan of
@@ -1823,8 +1871,8 @@ extern "C" int64_t dls_emit(int n, int symmetric, int fixed_first_row, int depth
     if ((rc = prepare(n, symmetric, fixed_first_row, depth, &prm, false))) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     u64 *d_stats = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&d_stats, DLS_STATS_WORDS * sizeof(u64), s);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    cudaError_t e = dls::scratch_alloc((void **)&d_stats, DLS_STATS_WORDS * sizeof(u64), s);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch_alloc");
     cudaMemsetAsync(d_stats, 0, DLS_STATS_WORDS * sizeof(u64), s);
     prm.prefixes = d_prefixes;
     prm.n_prefix = n_prefix;

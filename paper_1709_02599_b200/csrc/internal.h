@@ -1,6 +1,8 @@
 // internal.h -- host-side helpers shared by the product's C++/CUDA sources.
 // (Product side only; the oracle under oracle/ shares nothing with this.)
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -47,8 +49,10 @@ bool valid_record(const Plan &plan, int depth, const uint8_t *rec);
 // dls_count for an arbitrary plan (count.cu).
 // Records are refined on the host (P:481 below each record) when fewer than
 // refine_below (< 0: the default, ~1 per lane) are given.
-// Keep freed memory of the device's default stream-ordered pool cached (once).
-void keep_pool_memory(int dev);
+// Scratch device memory from the library's own stream-ordered pool (one per
+// device, freed memory kept cached up to 1 GB); free with cudaFreeAsync.
+cudaError_t scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream);
+void scratch_trim(size_t keep_bytes);
 int count_records(const Plan &plan, int depth, const uint8_t *prefix_buf, int64_t n_prefix, uint64_t *out_counts,
                   uint64_t *out_total, uint64_t *out_nodes, void *stream, int64_t refine_below = -1);
 

@@ -30,6 +30,8 @@
 // 768 for vertically symmetric N = 10.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -69,6 +71,7 @@ struct SbParams {
     int vs;
     int group;                         // number of transformations
     int mirror_choices;                // 2 (DLS) or 1 (VS)
+    int soff;                          // offset of order n's sigma tables
     int k_last;                        // free left-half cells of row N-1 (planned)
     uint8_t last_cols[16];             // their columns, in plan order
     uint8_t *out_rec;                  // canonic hourglasses (n*n bytes each)
@@ -85,8 +88,12 @@ struct SbParams {
 #define SB_CHECK(cond, k) do { } while (0)
 #endif
 
-__constant__ u64 c_sigma[kMaxGroup / 2];     // sigma as 4-bit fields (index -> image index)
-__constant__ u64 c_sigma_inv[kMaxGroup / 2];
+// The sigma tables of every order n = 3..10 (2^h (h-1)! entries each, h = n/2),
+// one after another: uploaded once per device and never rewritten, so calls on
+// different streams or threads can never see another order's group.
+constexpr int kSigmaTotal = 2 + 4 + 4 + 16 + 16 + 96 + 96 + 768;
+__constant__ u64 c_sigma[kSigmaTotal];       // sigma as 4-bit fields (index -> image index)
+__constant__ u64 c_sigma_inv[kSigmaTotal];
 
 __device__ __forceinline__ int nib(u64 w, int i) { return (int)((w >> (4 * i)) & 15ull); }
 
@@ -128,15 +135,16 @@ __device__ void image_key(int n, u64 D, u64 A, u64 B, u64 sg, u64 si, int mirror
 
 // Alg. 5: 0 if some image is lexicographically smaller (H not canonic), else the
 // class size |G| / |stabiliser|.
-__device__ uint32_t canonize_dab(int n, int group, int mirror_choices, u64 D, u64 A, u64 B) {
+__device__ uint32_t canonize_dab(int n, int group, int mirror_choices, int soff, u64 D, u64 A, u64 B) {
+    const u64 *const sig = c_sigma + soff, *const sinv = c_sigma_inv + soff;
     u64 h0, l0;
-    image_key(n, D, A, B, c_sigma[0], c_sigma_inv[0], 0, h0, l0);   // transformation 0 = identity
+    image_key(n, D, A, B, sig[0], sinv[0], 0, h0, l0);   // transformation 0 = identity
     uint32_t stab = 0;
     const int per_mirror = group / mirror_choices;
     for (int g = 0; g < per_mirror; ++g)
         for (int m = 0; m < mirror_choices; ++m) {
             u64 hi, lo;
-            image_key(n, D, A, B, c_sigma[g], c_sigma_inv[g], m, hi, lo);
+            image_key(n, D, A, B, sig[g], sinv[g], m, hi, lo);
             if (hi < h0 || (hi == h0 && lo < l0)) return 0u;
             if (hi == h0 && lo == l0) ++stab;
         }
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
     unsigned long long seen = 0, canon = 0;
     if (k == 0) {
         seen = 1;
-        const uint32_t m = canonize_dab(n, p.group, p.mirror_choices, D, A, B);
+        const uint32_t m = canonize_dab(n, p.group, p.mirror_choices, p.soff, D, A, B);
         if (m) canon = 1;
     } else {
         auto cand = [&](int l) {
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
             }
             if (lvl + 1 == k) {
                 ++seen;
-                const uint32_t m = canonize_dab(n, p.group, p.mirror_choices, D, A, B);
+                const uint32_t m = canonize_dab(n, p.group, p.mirror_choices, p.soff, D, A, B);
                 SB_CHECK(m == 0u || (uint32_t)p.group % m == 0u, 2);     // |G| / |Stab|
                 if (m) {
                     ++canon;
@@ -263,7 +271,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
         if ((long long)slot < p.capacity) {
             uint8_t *dst = p.out_rec + slot * (unsigned long long)(n * n);
             for (int c = 0; c < n * n; ++c) dst[c] = rec[c];
-            p.out_mult[slot] = canonize_dab(n, p.group, p.mirror_choices, D, A, B);
+            p.out_mult[slot] = canonize_dab(n, p.group, p.mirror_choices, p.soff, D, A, B);
         } else {
             atomicOr(p.counters + 2, 1ull);
         }
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(kSbThreads) hourglass_kernel(const SbParams p)
 
 // Canonise given hourglass records (for tests / external drivers).
 __global__ void __launch_bounds__(kSbThreads) canonize_kernel(const uint8_t *recs, long long n_rec, int n, int group,
-                                                              int mirror_choices, uint32_t *out) {
+                                                              int mirror_choices, int soff, uint32_t *out) {
     const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= n_rec) return;
     const uint8_t *rec = recs + w * (long long)n * n;
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(kSbThreads) canonize_kernel(const uint8_t *rec
         A |= (u64)rec[i * n + (n - 1 - i)] << (4 * i);
         B |= (u64)rec[(n - 1) * n + i] << (4 * i);
     }
-    out[w] = canonize_dab(n, group, mirror_choices, D, A, B);
+    out[w] = canonize_dab(n, group, mirror_choices, soff, D, A, B);
 }
 
 int fail(cudaError_t e, const char *what) {
@@ -292,12 +300,13 @@ int fail(cudaError_t e, const char *what) {
     return DLS_E_CUDA;
 }
 
-// The transformation group as sigma tables; returns |G| (sigma count x mirrors).
-int build_group(int n, bool vs, int *mirror_choices) {
+// sigma tables of order n: 2^h (h-1)! permutations of the rows/columns (pair
+// {0, n-1} kept in place, the other symmetric pairs permuted, each pair swapped
+// or not), identity first
+void sigma_tables(int n, std::vector<u64> &sg, std::vector<u64> &si) {
     const int h = n / 2;
     std::vector<int> pi(h);
     std::iota(pi.begin(), pi.end(), 0);
-    std::vector<u64> sg, si;
     do {
         for (int s = 0; s < (1 << h); ++s) {
             int sigma[16], inv[16];
@@ -316,11 +325,49 @@ int build_group(int n, bool vs, int *mirror_choices) {
             si.push_back(b);
         }
     } while (std::next_permutation(pi.begin() + 1, pi.end()));
-    // identity first (it is: pi = id, s = 0)
+}
+
+// Offset of order n's tables in c_sigma / c_sigma_inv.
+int sigma_offset(int n) {
+    int off = 0;
+    for (int m = 3; m < n; ++m) {
+        int h = m / 2, f = 1;
+        for (int k = 2; k < h; ++k) f *= k;
+        off += (1 << h) * f;
+    }
+    return off;
+}
+
+// Upload every order's tables to the current device, once (thread-safe).
+int upload_groups() {
+    static std::once_flag once[64];
+    static int status[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(e, "cudaGetDevice");
+    std::call_once(once[dev & 63], [&]() {
+        std::vector<u64> sg, si;
+        for (int n = 3; n <= DLS_MAX_ORDER; ++n) sigma_tables(n, sg, si);
+        cudaError_t e1 = sg.size() == (size_t)kSigmaTotal ? cudaSuccess : cudaErrorInvalidValue;
+        if (e1 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_sigma, sg.data(), sg.size() * sizeof(u64));
+        if (e1 == cudaSuccess) e1 = cudaMemcpyToSymbol(c_sigma_inv, si.data(), si.size() * sizeof(u64));
+        status[dev & 63] = (int)e1;
+    });
+    if (status[dev & 63] != (int)cudaSuccess) return fail((cudaError_t)status[dev & 63], "group tables");
+    return DLS_OK;
+}
+
+// The transformation group of order n: |G| (sigma count x mirrors), the mirror
+// choices and the tables' offset; DLS_E_CUDA if the tables could not be uploaded.
+int build_group(int n, bool vs, int *mirror_choices, int *soff) {
+    const int rc = upload_groups();
+    if (rc) return rc;
+    const int h = n / 2;
+    int f = 1;
+    for (int k = 2; k < h; ++k) f *= k;
     *mirror_choices = vs ? 1 : 2;
-    cudaMemcpyToSymbol(c_sigma, sg.data(), sg.size() * sizeof(u64));
-    cudaMemcpyToSymbol(c_sigma_inv, si.data(), si.size() * sizeof(u64));
-    return (int)sg.size() * *mirror_choices;
+    *soff = sigma_offset(n);
+    return (1 << h) * f * *mirror_choices;
 }
 
 bool device_ptr(const void *ptr) {
@@ -348,32 +395,30 @@ extern "C" int dls_canonize(int n, int symmetric, const uint8_t *hourglasses, in
     }
     if (n_rec == 0) return DLS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    int mirrors = 0;
-    const int group = build_group(n, symmetric, &mirrors);
+    int mirrors = 0, soff = 0;
+    const int group = build_group(n, symmetric, &mirrors, &soff);
+    if (group < 0) return group;
     cudaError_t e;
     const uint8_t *d_in = hourglasses;
     uint32_t *d_out = out_mult;
     void *tmp_in = nullptr, *tmp_out = nullptr;
     const size_t bytes = (size_t)n_rec * n * n;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dls::keep_pool_memory(dev);
     if (!device_ptr(hourglasses)) {
-        if ((e = cudaMallocAsync(&tmp_in, bytes, s)) != cudaSuccess) return fail(e, "cudaMallocAsync");
+        if ((e = dls::scratch_alloc(&tmp_in, bytes, s)) != cudaSuccess) return fail(e, "scratch_alloc");
         cudaMemcpyAsync(tmp_in, hourglasses, bytes, cudaMemcpyHostToDevice, s);
         d_in = (const uint8_t *)tmp_in;
     }
     const bool host_out = !device_ptr(out_mult);
     if (host_out) {
-        if ((e = cudaMallocAsync(&tmp_out, (size_t)n_rec * 4, s)) != cudaSuccess) {
+        if ((e = dls::scratch_alloc(&tmp_out, (size_t)n_rec * 4, s)) != cudaSuccess) {
             if (tmp_in) cudaFreeAsync(tmp_in, s);
             cudaStreamSynchronize(s);
-            return fail(e, "cudaMallocAsync");
+            return fail(e, "scratch_alloc");
         }
         d_out = (uint32_t *)tmp_out;
     }
     canonize_kernel<<<(unsigned)((n_rec + kSbThreads - 1) / kSbThreads), kSbThreads, 0, s>>>(d_in, n_rec, n, group,
-                                                                                             mirrors, d_out);
+                                                                                             mirrors, soff, d_out);
     e = cudaGetLastError();
     if (e == cudaSuccess && host_out) e = cudaMemcpyAsync(out_mult, d_out, (size_t)n_rec * 4, cudaMemcpyDeviceToHost, s);
     if (tmp_in) cudaFreeAsync(tmp_in, s);
@@ -411,7 +456,8 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
     sp.vs = symmetric;
     sp.k_last = hd - dd;
     for (int l = 0; l < sp.k_last; ++l) sp.last_cols[l] = (uint8_t)(hg.cells[dd + l] % n);
-    sp.group = build_group(n, symmetric, &sp.mirror_choices);
+    sp.group = build_group(n, symmetric, &sp.mirror_choices, &sp.soff);
+    if (sp.group < 0) return sp.group;
     // diagonal workunits (host split), the range [diag_begin, diag_end) of them,
     // processed in chunks to bound memory
     const int64_t n_all = dls_split(n, symmetric, 1, dd, nullptr, 0);
@@ -436,15 +482,13 @@ extern "C" int dls_count_sb_range(int n, int symmetric, int64_t diag_begin, int6
         for (void *q : {(void *)d_diag, (void *)d_rec, (void *)d_mult, (void *)d_cnt})
             if (q) cudaFreeAsync(q, s);
         cudaStreamSynchronize(s);
+        dls::scratch_trim((size_t)64 << 20);   // keep the search's small scratch, not ours
     };
-    // scratch from the stream-ordered pool (kept cached across calls)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dls::keep_pool_memory(dev);
-    if ((e = cudaMallocAsync((void **)&d_diag, (size_t)std::min<int64_t>(n_diag, chunk) * nn + 1, s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void **)&d_rec, (size_t)cap * nn, s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void **)&d_mult, (size_t)cap * 4, s)) != cudaSuccess ||
-        (e = cudaMallocAsync((void **)&d_cnt, 4 * sizeof(unsigned long long), s)) != cudaSuccess) {
+    // scratch from the library's stream-ordered pool
+    if ((e = dls::scratch_alloc((void **)&d_diag, (size_t)std::min<int64_t>(n_diag, chunk) * nn + 1, s)) != cudaSuccess ||
+        (e = dls::scratch_alloc((void **)&d_rec, (size_t)cap * nn, s)) != cudaSuccess ||
+        (e = dls::scratch_alloc((void **)&d_mult, (size_t)cap * 4, s)) != cudaSuccess ||
+        (e = dls::scratch_alloc((void **)&d_cnt, 4 * sizeof(unsigned long long), s)) != cudaSuccess) {
         cleanup();
         return fail(e, "cudaMalloc");
     }

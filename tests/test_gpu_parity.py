@@ -440,3 +440,60 @@ def test_closure_dls8_sample_and_nodes():
     counts, _, nodes = _gpu(n, False, recs, d)
     want, want_nodes = _oracle_per_prefix(n, False, recs, d)
     assert (counts == want).all() and nodes == want_nodes
+
+
+def test_closure_event_count_in_stats():
+    """stats[8] = two-row states counted in closed form = the oracle's number of
+    consistent partial squares at the closure level (every one is an event)."""
+    import torch
+    n, vs = 7, False
+    d = D.default_split_depth(n, vs)
+    recs = D.dls_split(n, d, vs)
+    levels = D.dls_search_levels(n, d, vs)
+    order = oracle.plan(n, vs)[d:]
+    assert levels < len(order)
+    want = sum(oracle.count_levels(n, vs, synth.to_int_grid(r), order)[1][levels - 1] for r in recs)
+    dev = torch.from_numpy(recs).cuda()
+    stats = torch.zeros(B.DLS_STATS_WORDS, dtype=torch.int64, device="cuda")
+    D.dls_count_async(n, d, dev, None, stats, vs, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    st = stats.cpu().tolist()
+    assert st[8] == want and st[0] == oracle.count_all(n)
+
+
+def _children(tag, n):
+    idx, recs, cnt, nodes, nodes2 = [], [], [], [], []
+    extra = None
+    for line in open(golden("children_%s.txt" % tag)):
+        if line.startswith("#"):
+            if "random descent of" in line:
+                extra = int(line.split("random descent of")[1].split()[0])
+            continue
+        i, r, c, nd, nd2 = line.split()
+        idx.append(int(i))
+        recs.append([255 if ch == "." else int(ch) for ch in r])
+        cnt.append(int(c))
+        nodes.append(int(nd))
+        nodes2.append(int(nd2))
+    return idx, np.array(recs, np.uint8).reshape(-1, n, n), np.array(cnt, np.uint64), sum(nodes), sum(nodes2), extra
+
+
+@pytest.mark.parametrize("tag,n,vs,seed,count", [("vs10", 10, True, synth.SEED_VS10, synth.N_VS10),
+                                                 ("dls9", 9, False, synth.SEED_DLS9, synth.N_DLS9)])
+def test_every_seeded_prefix_has_an_oracle_checked_child(tag, n, vs, seed, count):
+    """Configs 4/5: for EVERY one of the seeded prefixes, one seeded-random child
+    (scripts/make_golden_children.py, oracle only) -- the GPU count of each child
+    equals the oracle's; nodes equal the oracle's two-row-level nodes (closure on)
+    and its full-tree nodes (closure off); each child extends its seeded prefix."""
+    idx, kids, want, nodes_full, nodes_two, extra = _children(tag, n)
+    assert idx == list(range(count))
+    pre = synth.diagonal_prefixes(seed, n, count, vs=vs)
+    given = pre != 255
+    assert (kids[given] == pre[given]).all()
+    d = D.default_split_depth(n, vs) + extra
+    counts, total, nodes = _gpu(n, vs, kids, d)
+    assert (counts == want).all()
+    assert nodes == nodes_two
+    with closure_off():
+        counts0, _, nodes0 = _gpu(n, vs, kids, d)
+    assert (counts0 == want).all() and nodes0 == nodes_full

@@ -203,3 +203,19 @@ def test_cli_host_commands():
     out = subprocess.run([sys.executable, "-m", "paper_1709_02599_b200", "split", "--n", "8", "--depth", "14"],
                          capture_output=True, text=True, cwd=ROOT)
     assert out.stdout.strip() == "547896"
+
+
+def test_binding_validates_buffers():
+    """Marshalling guards (no GPU needed: they run before the C call): records must
+    be uint8 (k, n, n); counts 8-byte integers with room for every record."""
+    recs = np.zeros((4, 7, 7), np.uint8)
+    with pytest.raises(ValueError):
+        B.dls_count(7, 11, recs.astype(np.int32))
+    with pytest.raises(ValueError):
+        B.dls_count(7, 11, np.zeros((4, 6, 6), np.uint8))
+    with pytest.raises(ValueError):
+        B.dls_count(7, 11, recs, out_counts=np.zeros(4, np.int32))
+    with pytest.raises(ValueError):
+        B.dls_count(7, 11, recs, out_counts=np.zeros(3, np.uint64))
+    with pytest.raises(ValueError):
+        B.dls_emit(7, 11, recs, np.zeros((5, 49), np.int8))

@@ -178,3 +178,23 @@ def test_gpu_count_sb_ranges_add_up():
     parts = [D.dls_count_sb_range(n, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
     for key in ("count", "hourglasses", "classes"):
         assert sum(p[key] for p in parts) == full[key]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,vs,world,chunk", [(7, False, 3, 5), (8, False, 2, 20000), (8, True, 4, 3)])
+def test_gpu_count_sb_round_robin_shards(n, vs, world, chunk):
+    """The multi-GPU split of Alg. 6 (paper_1709_02599_b200.dist.shard_ranges):
+    diagonal-workunit ranges dealt round-robin to `world` ranks; the ranks'
+    dls_count_sb_range totals add up to dls_count_sb (run here one rank after
+    the other on one GPU; the all-reduce is covered by the gloo test)."""
+    from paper_1709_02599_b200.dist import shard_ranges
+    full = D.dls_count_sb(n, vs)
+    d = D.default_split_depth(n, vs)
+    n_units = len(D.dls_split(n, d, vs))
+    tot = {"count": 0, "hourglasses": 0, "classes": 0}
+    for r in range(world):
+        for b, e in shard_ranges(n_units, r, world, chunk):
+            part = D.dls_count_sb_range(n, b, e, vs)
+            for k in tot:
+                tot[k] += part[k]
+    assert tot == {k: full[k] for k in tot}
