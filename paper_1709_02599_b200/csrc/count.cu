@@ -754,6 +754,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
     const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per queue slot
     uint32_t *const lanecnt = reinterpret_cast<uint32_t *>(cq_mem + LY::CQ * CQSTR);
+    uint32_t *const scratch = lanecnt + NT;        // 32 words per warp (close_pass)
     const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
     const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * (uint32_t)CL::EW * 4u;
     uint32_t cq_w = cq_lane0;          // shared address of this lane's next queue entry
@@ -762,7 +763,6 @@ dls_search_kernel(const __grid_constant__ Params p) {
     constexpr bool kCqShift = LY::NT_FIXED != 0;
     constexpr int kCqLog = LY::NT_FIXED == 1024 ? (CL::EW == 4 ? 14 : 15) : 0;
     static_assert(!kCqShift || (1 << kCqLog) == LY::NT_FIXED * CL::EW * 4, "queue slot stride");
-    uint32_t cq_rot = 0;               // first lane of the next pass (round robin)
     const uint32_t rsel = (uint32_t)p.cl_rword;
     if (CLOSE) lanecnt[tid] = 0u;
 
@@ -820,39 +820,38 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // credits the completions to the lane that raised it, and every lane drops
     // the events taken from its queue (an emptied queue restarts at slot 0).
     auto close_pass = [&]() {
+        // the events are taken round by round -- every lane's oldest pending
+        // event, then every lane's second oldest, ... -- up to 32; the lane with
+        // rank k in that order writes (its id, its queue slot) to word k of the
+        // warp's scratch, and lane k evaluates that event
         const int c = cq_n - cq_r;
-        // lanes in round-robin order starting at cq_rot, so that no queue waits long
-        const int rl = (lane - (int)cq_rot) & 31;           // rank of this lane
-        int inc = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int v = __shfl_sync(kFull, inc, (lane - d) & 31);
-            if (rl >= d) inc += v;
+        uint32_t *const slotw = scratch + (tid - lane);
+        int filled = 0, mine = 0;
+#pragma unroll 1
+        for (int r = 0; r < LY::CQ && filled < 32; ++r) {
+            const unsigned b = __ballot_sync(kFull, c > r);
+            if (!b) break;
+            const int rank = filled + __popc(b & lt_mask);
+            if (c > r && rank < 32) {
+                slotw[rank] = (uint32_t)lane << 8 | (uint32_t)(cq_r + r);
+                ++mine;
+            }
+            filled += __popc(b);
         }
-        const int pex = inc - c;
-        const int total = __shfl_sync(kFull, inc, (int)(cq_rot + 31u) & 31);
-        int sr = 0;                                          // rank of the source lane
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-            const int v = __shfl_sync(kFull, pex, (sr + d + (int)cq_rot) & 31);
-            if (v <= lane) sr += d;
-        }
-        const int src = (sr + (int)cq_rot) & 31;
-        const int s_pex = __shfl_sync(kFull, pex, src);
-        const uint32_t s_addr = __shfl_sync(kFull, cq_lane0 + (uint32_t)cq_r * CQSTR, src);
         __syncwarp();
-        if (lane < total) {
+        if (lane < filled) {
+            const uint32_t v = slotw[lane];
+            const int src = (int)(v >> 8);
             const uint32_t *e = reinterpret_cast<const uint32_t *>(
-                cq_mem + (s_addr - cq_sa) + (uint32_t)(lane - s_pex) * CQSTR);
+                cq_mem + (v & 255u) * CQSTR + (uint32_t)(tid - lane + src) * (uint32_t)CL::EW * 4u);
             const uint32_t k = CL::eval(e, p, rsel);
             if (k) atomicAdd(lanecnt + (tid - lane) + src, k);
         }
         __syncwarp();
-        cq_r += max(0, min(32 - pex, c));
+        cq_r += mine;
         if (cq_r == cq_n) { cq_r = cq_n = 0; cq_w = cq_lane0; }
-        cq_rot = (cq_rot + 7u) & 31u;
-        if (lane == 0) acc[6] += (u64)min(total, 32);
-        return total;
+        if (lane == 0) acc[6] += (u64)min(filled, 32);
+        return filled;
     };
     auto close_drain = [&]() {
         while (__reduce_add_sync(kFull, (unsigned)(cq_n - cq_r)) != 0u) close_pass();
@@ -1154,19 +1153,19 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 // queue -- two predicated instructions, no branch, no vote
                 const uint4 w = CL::pack(st, rsel);
                 if constexpr (Geo<N, VS>::LAYOUT != 4) {
-                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %0, %1;\n\t"
-                                 "@ev st.shared.v4.u32 [%2], {%3, %4, %5, %6};\n\t}"
-                                 :: "r"(nl), "r"(L), "r"(cq_w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w));
+                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %1, %2;\n\t"
+                                 "@ev st.shared.v4.u32 [%0], {%4, %5, %6, %7};\n\t"
+                                 "@ev add.u32 %0, %0, %3;\n\t}"
+                                 : "+r"(cq_w) : "r"(nl), "r"(L), "r"(CQSTR), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w));
                 } else {
-                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %0, %1;\n\t"
-                                 "@ev st.shared.v4.u32 [%2], {%3, %4, %5, %6};\n\t"
-                                 "@ev st.shared.u32 [%2+16], %7;\n\t}"
-                                 :: "r"(nl), "r"(L), "r"(cq_w), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w),
-                                    "r"(CL::pack_row(st, rsel)));
+                    asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.s32 ev, %1, %2;\n\t"
+                                 "@ev st.shared.v4.u32 [%0], {%4, %5, %6, %7};\n\t"
+                                 "@ev st.shared.u32 [%0+16], %8;\n\t"
+                                 "@ev add.u32 %0, %0, %3;\n\t}"
+                                 : "+r"(cq_w) : "r"(nl), "r"(L), "r"(CQSTR), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w),
+                                   "r"(CL::pack_row(st, rsel)));
                 }
-                const bool ev = nl > L;
-                cq_w += ev ? CQSTR : 0u;
-                if constexpr (!kCqShift) cq_n += ev ? 1 : 0;
+                if constexpr (!kCqShift) cq_n += nl > L ? 1 : 0;
             }
         }
             if constexpr (CLOSE) {
@@ -1511,7 +1510,7 @@ size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close) {
     if (!close) return base;
     const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
     const size_t cq = lay == 0 ? 9 : (lay == 1 ? 7 : 6);     // Layout::CQ
-    return base + cq * nthreads * ew * 4 + (size_t)nthreads * 4;   // queues + counters
+    return base + cq * nthreads * ew * 4 + (size_t)nthreads * 8;   // queues + counters + pass scratch
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
