@@ -142,6 +142,12 @@ struct Params {
     // leaves): read entry (words 4..7) and toggle entry (words 0..7) of each
     int cl_nf;
     Tab cl_fread[2], cl_ftog[2];
+    // lookahead (Section 2.4.2; LOOK kernels, DLS N = 9): after the
+    // toggle of transition t also read the candidates of a watched cell; none
+    // left -> the branch is cut.  look_sel[t + 1] = its row / column selectors
+    // (transitions without a watched cell watch cell(t+1) itself: a no-op)
+    int look;
+    uint32_t look_sel[kMaxLevels + 2][2];
     uint8_t level_cell[kMaxLevels + 2];   // cell (i*n+j) of level l = 1..L
     Tab tab[kMaxLevels + 2]; // tab[t + 1], t = -1 .. L
 };
@@ -733,13 +739,20 @@ __device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, 
 }
 
 
-template <int N, bool VS, bool EMIT, bool CLOSE>
-__global__ void __launch_bounds__(1024, 1)
+// lanes per CTA at most: 1024 for the byte / word-field layouts; 896 for the
+// 9- / 10-bit-field layouts, whose larger state needs up to 72 registers
+__host__ __device__ constexpr int max_lanes(int layout) { return layout < 2 ? 1024 : 896; }
+
+template <int N, bool VS, bool EMIT, bool CLOSE, bool LOOK = false>
+__global__ void __launch_bounds__(max_lanes(Geo<N, VS>::LAYOUT), 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
     typedef typename M::CT CT;
     typedef Layout<N, VS> LY;
     typedef Close<N, VS> CL;
+    // table block of a transition: 32 toggle entries, 32 read entries (16-byte
+    // lane stride), then (LOOK) 32 watched-cell entries of 8 bytes
+    constexpr int BLKW = LY::BLK_WORDS + (LOOK ? 64 : 0);
     extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
     const int NT = LY::NT_FIXED ? LY::NT_FIXED : (int)blockDim.x;
@@ -747,7 +760,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     typedef typename LY::SW SW;
-    char *const stk = reinterpret_cast<char *>(smem + (L + 2) * LY::BLK_WORDS);
+    char *const stk = reinterpret_cast<char *>(smem + (L + 2) * BLKW);
     // closure queues ([slot][lane], Close::EW words per entry) and the per-lane
     // completion counters they feed, after the stack (16-byte aligned)
     const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)NT * (uint32_t)sizeof(SW);
@@ -768,9 +781,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
 
     for (int k = tid; k < (L + 2) * 32; k += NT) {
         const Tab &e = p.tab[k >> 5];
-        uint32_t *const blk = smem + (k >> 5) * LY::BLK_WORDS;
+        uint32_t *const blk = smem + (k >> 5) * BLKW;
         reinterpret_cast<uint4 *>(blk)[k & 31] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
         reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+        if (LOOK) reinterpret_cast<uint2 *>(blk + 256)[k & 31] = make_uint2(p.look_sel[k >> 5][0], p.look_sel[k >> 5][1]);
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
@@ -780,10 +794,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
     S[NT] = 0u;
     __syncthreads();
     // transition t: Fl[t * kBlk] (toggle part), Cl at +512 bytes (read part)
-    constexpr int kBlk = LY::BLK_WORDS / 4;                  // block stride in uint4 units
+    constexpr int kBlk = BLKW / 4;                  // block stride in uint4 units
 
-    const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + LY::BLK_WORDS) + lane;
-    const CT *const Cl = reinterpret_cast<const CT *>(smem + LY::BLK_WORDS + 128 + 4 * lane);
+    const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + BLKW) + lane;
+    const CT *const Cl = reinterpret_cast<const CT *>(smem + BLKW + 128 + 4 * lane);
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte view for t-offsets
 
     uint32_t *const pool = p.pool;
@@ -794,7 +808,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         atomicAdd(pool + 4, 1u);                   // ... and registered
         stamp_first(pool, kStampStart);
     }
-    bool waiting = false;
+    // (lane 0's acc[5] != 0 marks the warp as waiting: it holds the back-off)
 
     M st;
     st.clear();
@@ -805,7 +819,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // per-warp accumulators (shared memory, written by lane 0 / shared atomics):
     // [0] squares, [1] nodes, [2] donations, [3] busy lane-bursts,
     // [4] lane-bursts -- keeps them out of the registers of the search loop
-    // [5] (lane 0 only): ns between pool polls of this warp while idle
+    // [5] (lane 0 only): ns between pool polls of this warp while idle (0: not waiting)
     // [6] closure events evaluated
     __shared__ u64 wacc[32][7];
     u64 *const acc = wacc[tid >> 5];
@@ -908,7 +922,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 // device-wide pool, or leave once no warp is active and none is pending
                 uint32_t got = 0, h0 = 0, done = 0;
                 if (lane == 0) {
-                    if (!waiting) {
+                    if (acc[5] == 0) {               // not yet counted as waiting
                         atomicAdd(pool + 1, 1u);
                         __threadfence();
                         atomicSub(pool + 0, 1u);
@@ -941,7 +955,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 h0 = __shfl_sync(kFull, h0, 0);
                 done = __shfl_sync(kFull, done, 0);
                 if (done) break;
-                waiting = got == 0;
+                if (got && lane == 0) acc[5] = 0;    // active again
                 if (!got) {
                     if (lane == 0) {
                         const uint32_t ns = (uint32_t)acc[5];
@@ -1121,7 +1135,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 if (dn) sl[NT] = cur;                      // push L of level lvl
                 if (mv) sl[0] = sibs;
             }
-            const int toff = t * (LY::BLK_WORDS * 4);     // byte offset of transition t
+            const int toff = t * (BLKW * 4);     // byte offset of transition t
             const char *const tp = Fb + toff;              // one address for both parts
             const uint4 f = *reinterpret_cast<const uint4 *>(tp);
             const CT cs = *reinterpret_cast<const CT *>(tp + 512);
@@ -1133,7 +1147,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 const uint32_t d = dn ? b : sb - bb;                              // mark / unmark
                 st.toggle_d(f, d, d);
             }
-            const uint32_t c = st.cand(cs);               // AllN ^ (Rows | Columns) of cell(t+1)
+            uint32_t c = st.cand(cs);                     // AllN ^ (Rows | Columns) of cell(t+1)
+            if constexpr (LOOK) {
+                // lookahead: a watched cell left without candidates cuts the branch
+                const uint2 lk = *reinterpret_cast<const uint2 *>(tp + 1024);
+                const uint32_t cw = st.cand(make_uint4(0u, 0u, lk.x, lk.y));
+                c = cw ? c : 0u;
+            }
             const bool adv = dn || mv;
             const int nl = max(t + (adv ? 1 : 0), 0);
             // level L+1 is virtual: reaching it completes a square (P:93
@@ -1214,12 +1234,15 @@ dls_search_kernel(const __grid_constant__ Params p) {
 typedef void (*KernelFn)(Params);
 
 template <int N, bool VS>
-KernelFn kernel_for(bool emit, bool close) {
+KernelFn kernel_for(bool emit, bool close, bool look = false) {
+    if constexpr (N == 9 && !VS) {
+        if (look && !emit) return close ? dls_search_kernel<N, VS, false, true, true> : dls_search_kernel<N, VS, false, false, true>;
+    }
     return emit ? dls_search_kernel<N, VS, true, false>
                 : (close ? dls_search_kernel<N, VS, false, true> : dls_search_kernel<N, VS, false, false>);
 }
 
-KernelFn pick_kernel(int n, bool vs, bool emit, bool close) {
+KernelFn pick_kernel(int n, bool vs, bool emit, bool close, bool look) {
     switch (n) {
         case 1: return kernel_for<1, false>(emit, close);
         case 2: return vs ? kernel_for<2, true>(emit, close) : kernel_for<2, false>(emit, close);
@@ -1229,7 +1252,7 @@ KernelFn pick_kernel(int n, bool vs, bool emit, bool close) {
         case 6: return vs ? kernel_for<6, true>(emit, close) : kernel_for<6, false>(emit, close);
         case 7: return kernel_for<7, false>(emit, close);
         case 8: return vs ? kernel_for<8, true>(emit, close) : kernel_for<8, false>(emit, close);
-        case 9: return kernel_for<9, false>(emit, close);
+        case 9: return kernel_for<9, false>(emit, close, look);
         case 10: return vs ? kernel_for<10, true>(emit, close) : kernel_for<10, false>(emit, close);
         default: return nullptr;
     }
@@ -1476,6 +1499,32 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm, bool allow_close
     }
     std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.begin() + depth + prm->L);
     fill_tab(n, symmetric, level_cells, prm->tab);
+    // lookahead, DLS N = 9 only, opt-in: DLS_LOOKAHEAD=a-b applies it
+    // after the plan steps a..b (1-based, Fig. 1 numbering; the paper: 51-60).
+    // The watched cell of a step assigning (i, j) is the first later plan cell
+    // (after the next one) in row i or column j.
+    if (const char *la = getenv("DLS_LOOKAHEAD")) {
+        int a = 0, b = -1;
+        if (n == 9 && !symmetric && layout_of(n, symmetric) == 3 && sscanf(la, "%d-%d", &a, &b) == 2 && a <= b) {
+            prm->look = 1;
+            for (int t = -1; t <= prm->L; ++t) {
+                prm->look_sel[t + 1][0] = prm->tab[t + 1].w[6];   // default: cell(t+1) itself
+                prm->look_sel[t + 1][1] = prm->tab[t + 1].w[7];
+                const int step = depth + t;                        // plan step of cell(t), 1-based
+                if (t < 1 || t >= prm->L || step < a || step > b) continue;
+                const int c0 = plan.cells[depth + t - 1], i0 = c0 / n, j0 = c0 % n;
+                for (size_t q = depth + t + 1; q < plan.cells.size(); ++q) {
+                    const int c = plan.cells[q];
+                    if (c / n != i0 && c % n != j0) continue;
+                    Tab t3[3];
+                    fill_tab(n, symmetric, std::vector<int>{c}, t3);
+                    prm->look_sel[t + 1][0] = t3[1].w[6];
+                    prm->look_sel[t + 1][1] = t3[1].w[7];
+                    break;
+                }
+            }
+        }
+    }
     for (size_t l = 0; l < level_cells.size(); ++l) prm->level_cell[l + 1] = (uint8_t)level_cells[l];
     // assigned-cell pattern of a depth-`depth` prefix
     auto set = [&](int c) { prm->pat[c >> 6] |= 1ull << (c & 63); };
@@ -1502,11 +1551,11 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm, b
     return prepare_plan(plan, depth, prm, allow_close);
 }
 
-size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close) {
+size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close, bool look = false) {
     const int lay = layout_of(n, vs);
     const size_t sw = lay == 0 ? 1 : 2;                       // Layout::SW
     const size_t stack = (size_t)(L + 1 + 4 / sw) * nthreads * sw;
-    const size_t base = (size_t)(L + 2) * 32 * 32 + ((stack + 15) & ~(size_t)15);
+    const size_t base = (size_t)(L + 2) * (look ? 40 : 32) * 32 + ((stack + 15) & ~(size_t)15);
     if (!close) return base;
     const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
     const size_t cq = lay == 0 ? 9 : (lay == 1 ? 7 : 6);     // Layout::CQ
@@ -1515,7 +1564,8 @@ size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close) {
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     const bool close = prm.close && prm.emit == nullptr;
-    KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr, close);
+    const bool look = prm.look && prm.emit == nullptr;
+    KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr, close, look);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
     cudaError_t e;
     int dev = 0, sms = 0, smem_max = 0;
@@ -1527,10 +1577,10 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     smem_max -= 2048;   // static shared memory of the kernel (per-warp accumulators, 1.75 KB)
     // one persistent CTA per SM with as many lanes as fit (multiple of 32, <= 1024)
     const int lay = layout_of(n, vs);
-    int nthreads = 1024;                   // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
+    int nthreads = max_lanes(lay);         // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
     // (a multiple of 64, so that the u16 stack's lanes keep distinct banks)
-    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, close) > (size_t)smem_max) nthreads -= 64;
-    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, close);
+    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, close, look) > (size_t)smem_max) nthreads -= 64;
+    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, close, look);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute");

@@ -1,0 +1,61 @@
+"""Summarise one ncu --set full report of the search kernel into the JSON that
+bench.py reads (profiles/r2_ncu_close.json), stamped with the sha256 prefix of
+csrc/count.cu so that bench.py drops the fields once the kernel source changes.
+
+    python scripts/ncu_json.py gpurun_out/prof.ncu-rep "source note" > profiles/r2_ncu_close.json
+"""
+import csv
+import hashlib
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "usecond": 1e-3,
+             "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6, "second": 1e3}
+    d = {}
+    for h, u, v in zip(rows[0], rows[1], rows[2]):
+        try:
+            d[h] = float(v.replace(",", "")) * scale.get(u, 1.0)
+        except ValueError:
+            d[h] = v
+    return d, rows[2][rows[0].index("Kernel Name")] if "Kernel Name" in rows[0] else ""
+
+
+def num(d, k):
+    return float(d[k])
+
+
+def main():
+    rep, note = sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else ""
+    d, kname = raw(rep)
+    sha = hashlib.sha256(open(os.path.join(ROOT, "paper_1709_02599_b200", "csrc", "count.cu"), "rb").read()).hexdigest()[:16]
+    out = {
+        "kernel": kname,
+        "source": note,
+        "count_cu_sha": sha,
+        "dram_read_bytes": int(num(d, "dram__bytes_read.sum")),
+        "dram_write_bytes": int(num(d, "dram__bytes_write.sum")),
+        "issue_slots_busy_pct": num(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "alu_pipe_pct": num(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+        "fma_pipe_pct": num(d, "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+        "smem_lsu_wavefronts_pct": num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+        "smem_wavefronts": int(num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")),
+        "smem_bank_conflicts": int(num(d, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")),
+        "local_loads": int(num(d, "sass__inst_executed_local_loads")),
+        "local_stores": int(num(d, "sass__inst_executed_local_stores")),
+        "duration_ms": num(d, "gpu__time_duration.sum"),
+        "active_threads_per_warp_inst": num(d, "smsp__thread_inst_executed_per_inst_executed.ratio"),
+    }
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
