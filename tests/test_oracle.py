@@ -82,6 +82,100 @@ def test_plan_puts_diagonals_first(n):
     assert set(order[:len(diag)]) == diag
 
 
+def _units_of(n, i, j):
+    """The uniqueness units through cell (i, j): row, column, and the
+    main diagonal / antidiagonal when the cell lies on them."""
+    out = [[(i, k) for k in range(n)], [(k, j) for k in range(n)]]
+    if i == j:
+        out.append([(k, k) for k in range(n)])
+    if i + j == n - 1:
+        out.append([(k, n - 1 - k) for k in range(n)])
+    return out
+
+
+def _all_units(n):
+    """Rows 0..N-1, columns 0..N-1, main diagonal, antidiagonal (R5 scan order)."""
+    return ([[(i, k) for k in range(n)] for i in range(n)] + [[(k, j) for k in range(n)] for j in range(n)]
+            + [[(k, k) for k in range(n)], [(k, n - 1 - k) for k in range(n)]])
+
+
+@pytest.mark.parametrize("n", [4, 6, 8, 10])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_vs_plan_replay_against_section_2_3(n, fixed):
+    """Pin of the vertically symmetric plan (reading R4) by replaying it on a
+    board, checked against the text of Section 2.3 rather than the planner:
+      * every step takes a left-half cell ("fill only the left half") that
+        is still empty together with its mirror, and marks both;
+      * forced rule: when some unit has exactly N-1 assigned cells, the
+        step takes that unit's remaining cell (or its mirror), the first such
+        unit in the R5 scan order;
+      * otherwise the step takes a left-half cell of the largest
+        V = r_i + c_j + md(i,j) + ad(i,j), the first in lexicographic order;
+      * with the first row fixed and N >= 6 the left-half diagonal cells come
+        first (for N = 4 the V rule itself interleaves row cells), and
+        the plan ends with every cell assigned."""
+    order = oracle.plan(n, True, _pre_rows(n, fixed))
+    a = np.zeros((n, n), dtype=int)
+    if fixed:
+        a[0, :] = 1
+    ndiag = sum(1 for i in range(n) for j in range(n // 2) if (i == j or i + j == n - 1) and not a[i, j])
+    for step, cell in enumerate(order):
+        i, j = divmod(cell, n)
+        m = n - 1 - j
+        assert 2 * j < n and not a[i, j] and not a[i, m], (step, i, j)
+        forced = None
+        for u in _all_units(n):
+            if sum(a[p] for p in u) == n - 1:
+                forced = next(p for p in u if not a[p])
+                break
+        if forced is not None:
+            assert forced in ((i, j), (i, m)), (step, forced, (i, j))
+        else:
+            def v(ii, jj):
+                return sum(sum(a[p] for p in u) for u in _units_of(n, ii, jj))
+            free = [(ii, jj) for ii in range(n) for jj in range(n) if 2 * jj < n and not a[ii, jj]]
+            best = max(v(*c) for c in free)
+            assert v(i, j) == best and (i, j) == min(c for c in free if v(*c) == best), (step, (i, j))
+        if fixed and n >= 6 and step < ndiag:
+            assert i == j or i + j == n - 1, (step, i, j)
+        a[i, j] = a[i, m] = 1
+    assert a.all()
+
+
+def _pre_rows(n, fixed):
+    pre = np.zeros((n, n), dtype=np.int32)
+    if fixed:
+        pre[0, :] = 1
+    return pre
+
+
+@pytest.mark.parametrize("n", range(4, 11))
+def test_dls_plan_replay_forced_rule(n):
+    """The non-symmetric plan replayed the same way: every step where some unit
+    has N-1 assigned cells takes the remaining cell of the first such unit
+    (R5 scan order), every other step a cell of maximal V."""
+    order = oracle.plan(n)
+    a = np.zeros((n, n), dtype=int)
+    a[0, :] = 1
+    nforced = 0
+    for cell in order:
+        i, j = divmod(cell, n)
+        assert not a[i, j]
+        forced = next((next(p for p in u if not a[p]) for u in _all_units(n) if sum(a[p] for p in u) == n - 1), None)
+        if forced is not None:
+            assert forced == (i, j)
+            nforced += 1
+        else:
+            def v(ii, jj):
+                return sum(sum(a[p] for p in u) for u in _units_of(n, ii, jj))
+            free = [(ii, jj) for ii in range(n) for jj in range(n) if not a[ii, jj]]
+            best = max(v(*c) for c in free)
+            assert v(i, j) == best and (i, j) == min(c for c in free if v(*c) == best)
+        a[i, j] = 1
+    # the last cell of rows 1..N-1 and of both diagonals at least (Fig. 1)
+    assert nforced >= n + 1
+
+
 def test_plan_forced_cells_are_forced():
     # P:154: a cell taken because its unit reached N-1 assigned cells really is
     # the last free cell of that unit at that step (replay check).
