@@ -799,6 +799,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + BLKW) + lane;
     const CT *const Cl = reinterpret_cast<const CT *>(smem + BLKW + 128 + 4 * lane);
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte view for t-offsets
+    // (LOOK) watched-cell entries: 8-byte lane stride after the 1024 bytes of the two parts
+    const char *const Lb = reinterpret_cast<const char *>(smem + BLKW + 256) + 8 * lane;
 
     uint32_t *const pool = p.pool;
 
@@ -1150,7 +1152,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             uint32_t c = st.cand(cs);                     // AllN ^ (Rows | Columns) of cell(t+1)
             if constexpr (LOOK) {
                 // lookahead: a watched cell left without candidates cuts the branch
-                const uint2 lk = *reinterpret_cast<const uint2 *>(tp + 1024);
+                const uint2 lk = *reinterpret_cast<const uint2 *>(Lb + toff);
                 const uint32_t cw = st.cand(make_uint4(0u, 0u, lk.x, lk.y));
                 c = cw ? c : 0u;
             }

@@ -207,6 +207,47 @@ def test_config5_dls9_children_vs_oracle():
         assert nodes == want_nodes
 
 
+class env_set:
+    """Environment knobs of the library (read at every call) for the calls inside."""
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("rng_la,close", [("51-60", "1"), ("51-60", "0"), ("30-60", "1"), ("20-72", "0")])
+def test_lookahead_dls9_never_changes_counts(rng_la, close):
+    """Section 2.4.2: the lookahead only cuts branches that cannot be
+    completed, so every per-prefix count stays the oracle's; the kernel with it
+    visits no more nodes than without."""
+    n = 9
+    r = synth.diagonal_prefixes(synth.SEED_DLS9, n, 1)[0]
+    d = D.default_split_depth(n)
+    order = oracle.plan(n)
+    extra = 10
+    kids = oracle.prefixes(n, False, synth.to_int_grid(r), order[d:], extra)
+    pick = np.random.default_rng(5).choice(len(kids), min(12, len(kids)), replace=False)
+    kid_recs = np.where(kids[pick] < 0, 255, kids[pick]).astype(np.uint8)
+    want, _ = _oracle_per_prefix(n, False, kid_recs, d + extra)
+    with env_set(DLS_CLOSE=close):
+        c0, _, nodes0 = _gpu(n, False, kid_recs, d + extra)
+        with env_set(DLS_LOOKAHEAD=rng_la):
+            c1, _, nodes1 = _gpu(n, False, kid_recs, d + extra)
+    assert (c0 == want).all() and (c1 == want).all()
+    assert nodes1 <= nodes0
+
+
 # ------------------------------------------------------------------ edge cases
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
