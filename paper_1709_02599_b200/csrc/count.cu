@@ -71,6 +71,33 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_ONE_STORE
 #define DLS_ONE_STORE 1
 #endif
+// DLS_UNIFIED=1 (default): byte layout (N <= 8), 1024 lanes: a transition block
+// and a stack slot are both 1024 bytes, so ONE register -- the shared address of
+// the lane's table entry of the current level -- stands for the level; table and
+// stack addresses are that register plus per-lane constants (4 level
+// instructions per step instead of 7).  0 = the generic step (A/B baseline).
+#ifndef DLS_UNIFIED
+#define DLS_UNIFIED 1
+#endif
+// DLS_READ8=1: the byte layout's 8-byte read entries at an 8-byte lane stride (2
+// shared-memory wavefronts instead of 4).  DLS_FMA_ADDS=1: the level / address
+// additions of the unified step are written as multiply-adds with a factor the
+// compiler cannot see (Params::one = 1), so they issue on the FMA pipe instead
+// of the half-rate ALU pipe, which binds the step (profiles/r2_ab_step.log).
+#ifndef DLS_READ8
+#define DLS_READ8 0
+#endif
+#ifndef DLS_FMA_ADDS
+#define DLS_FMA_ADDS 0
+#endif
+// DLS_STEP_V2=1: the unified step selects the L set it works on first (one
+// select, one lowest-bit isolation instead of two) -- fewer ALU-pipe instructions
+#ifndef DLS_STEP_V2
+#define DLS_STEP_V2 1
+#endif
+// A closure round (every lane evaluates its newest event) starts once this many
+// lanes of the warp hold one (A/B: profiles/r2_ab_close_min.log)
+constexpr int kCloseMinLanes = 24;
 constexpr int kMinDonateDepth = 6;  // do not donate subtrees shallower than this (and < L/3)
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
@@ -137,6 +164,9 @@ struct Params {
     int cl_rword;            // mask-layout word holding row r1's field
     int cl_rshift;           // bit offset of row r1's field in that word
     uint32_t cl_sel[10];     // field selectors of the columns of J (padded)
+    int cl_min;              // lanes of a warp holding an event that start an evaluation round
+    int cl_cq;               // event slots per lane (set by launch from the shared memory left)
+    uint32_t one;            // 1 (see DLS_FMA_ADDS)
     // forced cells just before the two-row level, assigned inside the closure
     // (their value is the one candidate their complete-but-one row or column
     // leaves): read entry (words 4..7) and toggle entry (words 0..7) of each
@@ -418,8 +448,9 @@ struct Masks<N, VS, 4> {
 // pair gives e_j = 0: two completions that differ in that column).
 //
 // A closure event stores the part of the state it needs (the column words and
-// the words holding row r1) in its lane's queue in shared memory; the warp
-// evaluates 32 queued events at a time, one per lane (Close::eval).  The host
+// the words holding row r1) on its lane's event stack in shared memory; once
+// enough lanes of the warp hold an event, every lane evaluates its newest one
+// (Close::eval) -- the same instructions in all lanes.  The host
 // lists the columns of J as layout-specific field selectors (cl_sel), padded to
 // EM entries with a complete column (its missing set is empty).
 template <int N, bool VS, int LAYOUT = Geo<N, VS>::LAYOUT>
@@ -705,12 +736,13 @@ struct Layout {
     // lane is still element s * NT of an SW array based at the lane's offset
     typedef typename std::conditional<Geo<N, VS>::LAYOUT == 0, uint8_t, uint16_t>::type SW;
     static constexpr int PACK = 4 / (int)sizeof(SW);
-    // closure queue (CLOSE kernels): CQ entries per lane, [slot][lane]; the warp
-    // checks the queues every GROUP steps and drains them all once some queue
-    // holds more than CQ - GROUP entries, so none can overflow
-    static constexpr int CQ = Geo<N, VS>::LAYOUT == 0 ? 9 : (Geo<N, VS>::LAYOUT == 1 ? 7 : 6);
+    // closure events (CLOSE kernels): a stack of up to cl_cq events per lane,
+    // [slot][lane] (cl_cq: as many slots as the launch's shared memory holds,
+    // kCqMin .. kCqMax).  The warp looks at the stacks every GROUP steps: once
+    // enough lanes hold an event, every lane evaluates (and pops) its newest
+    // one; a stack deeper than cl_cq - GROUP forces such rounds until none is,
+    // so no stack can overflow during the next group
     static constexpr int GROUP = Geo<N, VS>::LAYOUT == 0 ? 6 : 4;
-    static_assert(CQ > GROUP, "closure queue too small");
 };
 
 __host__ __device__ inline uint32_t stack_lane_offset(int t, int nt, int sw) {
@@ -761,29 +793,31 @@ dls_search_kernel(const __grid_constant__ Params p) {
     const unsigned lt_mask = (1u << lane) - 1u;
     typedef typename LY::SW SW;
     char *const stk = reinterpret_cast<char *>(smem + (L + 2) * BLKW);
-    // closure queues ([slot][lane], Close::EW words per entry) and the per-lane
-    // completion counters they feed, after the stack (16-byte aligned)
+    // closure event stacks ([slot][lane], Close::EW words per entry) after the
+    // stack (16-byte aligned)
     const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)NT * (uint32_t)sizeof(SW);
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
-    const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per queue slot
-    uint32_t *const lanecnt = reinterpret_cast<uint32_t *>(cq_mem + LY::CQ * CQSTR);
-    uint32_t *const scratch = lanecnt + NT;        // 32 words per warp (close_pass)
+    const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per slot
     const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
     const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * (uint32_t)CL::EW * 4u;
-    uint32_t cq_w = cq_lane0;          // shared address of this lane's next queue entry
-    int cq_n = 0, cq_r = 0;            // entries written / evaluated since the queue was last empty
-    // (with a compile-time lane count cq_n is recomputed from cq_w at the checks)
-    constexpr bool kCqShift = LY::NT_FIXED != 0;
-    constexpr int kCqLog = LY::NT_FIXED == 1024 ? (CL::EW == 4 ? 14 : 15) : 0;
-    static_assert(!kCqShift || (1 << kCqLog) == LY::NT_FIXED * CL::EW * 4, "queue slot stride");
+    uint32_t cq_w = cq_lane0;          // shared address of this lane's next event slot
+    // a lane's stack is deeper than k events iff cq_w > cq_lane0 + k * CQSTR
+    const uint32_t cq_high = cq_lane0 + (uint32_t)(p.cl_cq - LY::GROUP) * CQSTR;
+    const uint32_t cl_min = (uint32_t)p.cl_min;    // lanes holding an event that start a round
     const uint32_t rsel = (uint32_t)p.cl_rword;
-    if (CLOSE) lanecnt[tid] = 0u;
 
+    // byte layout: the 8-byte read entries sit at an 8-byte lane stride (2
+    // shared-memory wavefronts per warp instead of the 4 of a 16-byte stride);
+    // the other layouts' read entries are 16 bytes
+    constexpr bool kRead8 = DLS_READ8 && sizeof(CT) == 8;
     for (int k = tid; k < (L + 2) * 32; k += NT) {
         const Tab &e = p.tab[k >> 5];
         uint32_t *const blk = smem + (k >> 5) * BLKW;
         reinterpret_cast<uint4 *>(blk)[k & 31] = make_uint4(e.w[0], e.w[1], e.w[2], e.w[3]);
-        reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
+        if constexpr (kRead8)
+            reinterpret_cast<uint2 *>(blk + 128)[k & 31] = make_uint2(e.w[4], e.w[5]);
+        else
+            reinterpret_cast<uint4 *>(blk + 128)[k & 31] = make_uint4(e.w[4], e.w[5], e.w[6], e.w[7]);
         if (LOOK) reinterpret_cast<uint2 *>(blk + 256)[k & 31] = make_uint2(p.look_sel[k >> 5][0], p.look_sel[k >> 5][1]);
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
@@ -797,8 +831,18 @@ dls_search_kernel(const __grid_constant__ Params p) {
     constexpr int kBlk = BLKW / 4;                  // block stride in uint4 units
 
     const uint4 *const Fl = reinterpret_cast<const uint4 *>(smem + BLKW) + lane;
-    const CT *const Cl = reinterpret_cast<const CT *>(smem + BLKW + 128 + 4 * lane);
+    const CT *const Cl = reinterpret_cast<const CT *>(smem + BLKW + 128 + (kRead8 ? 2 : 4) * lane);
+    const char *const Cb = reinterpret_cast<const char *>(Cl);
     const char *const Fb = reinterpret_cast<const char *>(Fl);   // byte view for t-offsets
+    // unified-address step (DLS_UNIFIED): shared addresses of the lane's entry of
+    // transition 0 and of level L + 1, and the distance from a level's entry to
+    // the stack slot S[level * NT]
+    constexpr bool kUni = DLS_UNIFIED && Geo<N, VS>::LAYOUT == 0 && !LOOK && !EMIT && BLKW * 4 == 1024 &&
+                          LY::NT_FIXED == 1024 && sizeof(SW) == 1;
+    const uint32_t fl_sa = (uint32_t)__cvta_generic_to_shared(Fb);
+    const uint32_t x_last = fl_sa + ((uint32_t)L << 10);          // above it: level L + 1
+    const uint32_t d_stk = (uint32_t)__cvta_generic_to_shared(S) - fl_sa;
+    const uint32_t d_rd = (uint32_t)__cvta_generic_to_shared(Cb) - fl_sa;   // entry -> its read part
     // (LOOK) watched-cell entries: 8-byte lane stride after the 1024 bytes of the two parts
     const char *const Lb = reinterpret_cast<const char *>(smem + BLKW + 256) + 8 * lane;
 
@@ -830,47 +874,18 @@ dls_search_kernel(const __grid_constant__ Params p) {
     bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
-    // Evaluate up to 32 pending closure events of this warp, the oldest of each
-    // lane first, one per lane: lane i takes the i-th event of the concatenation
-    // of the lanes' queues (exclusive prefix sums + a binary search over them),
-    // credits the completions to the lane that raised it, and every lane drops
-    // the events taken from its queue (an emptied queue restarts at slot 0).
-    auto close_pass = [&]() {
-        // the events are taken round by round -- every lane's oldest pending
-        // event, then every lane's second oldest, ... -- up to 32; the lane with
-        // rank k in that order writes (its id, its queue slot) to word k of the
-        // warp's scratch, and lane k evaluates that event
-        const int c = cq_n - cq_r;
-        uint32_t *const slotw = scratch + (tid - lane);
-        int filled = 0, mine = 0;
-#pragma unroll 1
-        for (int r = 0; r < LY::CQ && filled < 32; ++r) {
-            const unsigned b = __ballot_sync(kFull, c > r);
-            if (!b) break;
-            const int rank = filled + __popc(b & lt_mask);
-            if (c > r && rank < 32) {
-                slotw[rank] = (uint32_t)lane << 8 | (uint32_t)(cq_r + r);
-                ++mine;
-            }
-            filled += __popc(b);
-        }
-        __syncwarp();
-        if (lane < filled) {
-            const uint32_t v = slotw[lane];
-            const int src = (int)(v >> 8);
-            const uint32_t *e = reinterpret_cast<const uint32_t *>(
-                cq_mem + (v & 255u) * CQSTR + (uint32_t)(tid - lane + src) * (uint32_t)CL::EW * 4u);
-            const uint32_t k = CL::eval(e, p, rsel);
-            if (k) atomicAdd(lanecnt + (tid - lane) + src, k);
-        }
-        __syncwarp();
-        cq_r += mine;
-        if (cq_r == cq_n) { cq_r = cq_n = 0; cq_w = cq_lane0; }
-        if (lane == 0) acc[6] += (u64)min(filled, 32);
-        return filled;
+    // One round: every lane holding an event evaluates and pops its newest one;
+    // the completions go to the lane's own counter.
+    auto close_round = [&](uint32_t &cnt_) {
+        const bool has = cq_w != cq_lane0;
+        if (has) cq_w -= CQSTR;
+        const uint32_t k = CL::eval(reinterpret_cast<const uint32_t *>(cq_mem + (cq_w - cq_sa)), p, rsel);
+        cnt_ += has ? k : 0u;
+        const unsigned b = __ballot_sync(kFull, has);
+        if (lane == 0) acc[6] += (u64)__popc(b);
     };
-    auto close_drain = [&]() {
-        while (__reduce_add_sync(kFull, (unsigned)(cq_n - cq_r)) != 0u) close_pass();
+    auto close_drain = [&](uint32_t &cnt_) {
+        while (__any_sync(kFull, cq_w != cq_lane0)) close_round(cnt_);
     };
 
     for (;;) {
@@ -878,10 +893,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         if (CLOSE) {
             // every pending event belongs to the lane's current workunit: settle
             // them before a lane can finish it or take another
-            close_drain();
-            __syncwarp();
-            cnt += lanecnt[tid];
-            lanecnt[tid] = 0u;
+            close_drain(cnt);
             if (pid >= 0 && cnt >= 0x80000000u) {
                 if (p.counts) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
                 atomicAdd(acc + 0, (u64)cnt);
@@ -1120,6 +1132,96 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if (lane == 0) { acc[3] += (u64)__popc(busy); acc[4] += 32; }
         }
         uint32_t cnt32 = 0, ent32 = 0;
+        if constexpr (kUni) {
+        // ---- unified-address step (same step as below, see DLS_UNIFIED)
+        asm volatile("" ::: "memory");           // the stack is accessed through asm from here
+        uint32_t xq = fl_sa + ((uint32_t)lvl << 10);   // entry of transition lvl == slot of level lvl-1 (+ d_stk)
+        // x + k on the FMA pipe (one * k + x) or as a plain add
+        const uint32_t one = DLS_FMA_ADDS ? p.one : 1u;
+        auto addk = [&](uint32_t x, uint32_t k) { return one * k + x; };
+        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? LY::GROUP : 8)) {
+#pragma unroll
+        for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
+            const bool dn = cur != 0u;
+            uint32_t sp;                                   // L of level lvl-1
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(one * d_stk + xq));
+            const uint32_t bb = sp & (0u - sp);            // its lowest bit: the value assigned there
+            const uint32_t sibs = sp - bb;                 // L &= L-1
+#if DLS_STEP_V2
+            // the level this step (re)assigns holds X: level lvl's candidates on a
+            // descend, the untried siblings of level lvl-1 otherwise; empty =
+            // plain backtrack.  One select, one lowest-bit isolation.
+            const uint32_t X = dn ? cur : sibs;
+            const bool adv = X != 0u;
+            const uint32_t x = X & (0u - X);
+            DLS_CHECK(xq >= fl_sa && xq <= fl_sa + ((uint32_t)(L + 1) << 10) && (!dn || xq <= fl_sa + ((uint32_t)L << 10)) &&
+                      (xq > fl_sa || !adv), kChkStep);
+            uint32_t xt = xq;                              // transition t = dn ? lvl : lvl - 1
+            if (!dn) xt = addk(xq, 0u - 1024u);
+#else
+            const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
+            const uint32_t sb = sibs & (0u - sibs);
+            const bool mv = !dn && sibs != 0u;
+            const bool adv = dn || mv;
+            const uint32_t X = dn ? cur : sibs;
+            DLS_CHECK(xq >= fl_sa && xq <= fl_sa + ((uint32_t)(L + 1) << 10) && (!dn || xq <= fl_sa + ((uint32_t)L << 10)) &&
+                      (xq > fl_sa || (!dn && !mv)), kChkStep);
+            const uint32_t xt = dn ? xq : addk(xq, 0u - 1024u);   // transition t = dn ? lvl : lvl - 1
+#endif
+            uint4 f;
+            uint2 cs;
+            asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(f.x), "=r"(f.y), "=r"(f.z), "=r"(f.w) : "r"(xt));
+            if constexpr (kRead8)
+                asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cs.x), "=r"(cs.y) : "r"(one * d_rd + xt));
+            else
+                asm("ld.shared.v2.u32 {%0, %1}, [%2+512];" : "=r"(cs.x), "=r"(cs.y) : "r"(xt));
+#if DLS_STEP_V2
+            if constexpr (VS) {
+                st.toggle(f, x, dn ? 0u : bb);             // mark / unmark
+            } else {
+                uint32_t d = x;
+                if (!dn) d = x - bb;
+                st.toggle_d(f, d, d);
+            }
+            const uint32_t c = st.cand(cs);
+            uint32_t xn = xt;                              // level nl = max(t + adv, 0)
+            if (adv) xn = addk(xt, 1024u);
+            xn = max(xn, fl_sa);
+#else
+            if constexpr (VS) {
+                st.toggle(f, dn ? b : sb, dn ? 0u : bb);
+            } else {
+                const uint32_t d = dn ? b : sb - bb;
+                st.toggle_d(f, d, d);
+            }
+            const uint32_t c = st.cand(cs);
+            const uint32_t xn = max(adv ? addk(xt, 1024u) : xt, fl_sa);   // level nl = max(t + adv, 0)
+#endif
+            if (adv) asm volatile("st.shared.u8 [%0], %1;" :: "r"(one * d_stk + xn), "r"(X));
+            if (!CLOSE) cnt32 += xn > x_last ? 1u : 0u;
+            ent32 += adv ? 1u : 0u;
+            cur = adv ? c : 0u;
+            xq = xn;
+            if constexpr (CLOSE) {
+                const uint4 w = CL::pack(st, rsel);
+                asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.u32 ev, %1, %2;\n\t"
+                             "@ev st.shared.v4.u32 [%0], {%4, %5, %6, %7};\n\t"
+                             "@ev mad.lo.u32 %0, %8, %3, %0;\n\t}"
+                             : "+r"(cq_w) : "r"(xn), "r"(x_last), "r"(CQSTR), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w), "r"(one));
+            }
+        }
+            if constexpr (CLOSE) {
+                const unsigned pk = (cq_w != cq_lane0 ? 1u : 0u) + (cq_w > cq_high ? 1024u : 0u);
+                unsigned red = __reduce_add_sync(kFull, pk);
+                if (red >= cl_min) {
+                    close_round(cnt32);
+                    while (__any_sync(kFull, cq_w > cq_high)) close_round(cnt32);
+                }
+            }
+        }
+        lvl = (int)((xq - fl_sa) >> 10);
+        asm volatile("" ::: "memory");
+        } else {
         for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? LY::GROUP : 8)) {
 #pragma unroll
         for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
@@ -1140,7 +1242,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const int toff = t * (BLKW * 4);     // byte offset of transition t
             const char *const tp = Fb + toff;              // one address for both parts
             const uint4 f = *reinterpret_cast<const uint4 *>(tp);
-            const CT cs = *reinterpret_cast<const CT *>(tp + 512);
+            const CT cs = *reinterpret_cast<const CT *>(kRead8 ? Cb + toff : tp + 512);
             if constexpr (Geo<N, VS>::LAYOUT >= 3) {
                 st.toggle_d(f, cs, dn ? b : sb - bb);                             // mark / unmark
             } else if constexpr (VS || Geo<N, VS>::LAYOUT == 2) {
@@ -1165,7 +1267,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 // slot nl in both cases: the address the next step loads from
                 if (adv) S[nl * NT] = (SW)(dn ? cur : sibs);
             }
-            if (!CLOSE) cnt32 += nl > L ? 1u : 0u;
+            if (!CLOSE) cnt32 += nl > L ? 1u : 0u;    // (CLOSE: the closure rounds add to cnt32)
             if (EMIT && nl > L) emit_square<N, VS, SW>(p, pid, S, NT);
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
@@ -1187,23 +1289,20 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                  : "+r"(cq_w) : "r"(nl), "r"(L), "r"(CQSTR), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w),
                                    "r"(CL::pack_row(st, rsel)));
                 }
-                if constexpr (!kCqShift) cq_n += nl > L ? 1 : 0;
             }
         }
             if constexpr (CLOSE) {
-                // evaluate full batches of 32; drain everything when some queue
-                // could overflow during the next group.  One reduction carries
-                // both: the pending events (< 1024) and 1024 per queue near full.
-                if constexpr (kCqShift) cq_n = (int)((cq_w - cq_lane0) >> kCqLog);
-                const unsigned pk = (unsigned)(cq_n - cq_r) + (cq_n > LY::CQ - LY::GROUP ? 1024u : 0u);
-                const unsigned red = __reduce_add_sync(kFull, pk);
-                if (red >= 1024u) {
-                    close_drain();
-                } else if (red >= 32u) {
-                    close_pass();
+                // one reduction carries both tests: lanes holding an event (< 1024)
+                // and 1024 per stack that could overflow during the next group
+                const unsigned pk = (cq_w != cq_lane0 ? 1u : 0u) + (cq_w > cq_high ? 1024u : 0u);
+                unsigned red = __reduce_add_sync(kFull, pk);
+                if (red >= cl_min) {
+                    close_round(cnt32);
+                    while (__any_sync(kFull, cq_w > cq_high)) close_round(cnt32);
                 }
             }
         }
+        }   // generic step
         cnt += cnt32;
         if (cnt >= 0x80000000u) {          // flush before 32 bits could overflow
             if (p.counts) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
@@ -1453,6 +1552,8 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
             if (open >> j & 1u) prm->cl_sel[k++] = sel(j);
         while (k < 10) prm->cl_sel[k++] = sel(pad);
         prm->close = 1;
+        prm->cl_min = kCloseMinLanes;
+        if (const char *e = getenv("DLS_CLOSE_MIN")) prm->cl_min = std::min(32, std::max(1, atoi(e)));   // tuning
         prm->cl_open = open;
         prm->cl_E = E;
         prm->cl_nf = nf;
@@ -1553,15 +1654,18 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm, b
     return prepare_plan(plan, depth, prm, allow_close);
 }
 
-size_t smem_bytes(int n, bool vs, int L, int nthreads, bool close, bool look = false) {
+// event slots per lane of the closure kernels: at least kCqMin (= the largest
+// GROUP + 2), at most kCqMax
+constexpr int kCqMin = 8, kCqMinWide = 6, kCqMax = 16;
+
+// shared memory of a launch; cq = event slots per lane (0: no closure)
+size_t smem_bytes(int n, bool vs, int L, int nthreads, int cq, bool look = false) {
     const int lay = layout_of(n, vs);
     const size_t sw = lay == 0 ? 1 : 2;                       // Layout::SW
     const size_t stack = (size_t)(L + 1 + 4 / sw) * nthreads * sw;
     const size_t base = (size_t)(L + 2) * (look ? 40 : 32) * 32 + ((stack + 15) & ~(size_t)15);
-    if (!close) return base;
     const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
-    const size_t cq = lay == 0 ? 9 : (lay == 1 ? 7 : 6);     // Layout::CQ
-    return base + cq * nthreads * ew * 4 + (size_t)nthreads * 8;   // queues + counters + pass scratch
+    return base + (size_t)cq * nthreads * ew * 4;             // event stacks
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
@@ -1581,8 +1685,14 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     const int lay = layout_of(n, vs);
     int nthreads = max_lanes(lay);         // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
     // (a multiple of 64, so that the u16 stack's lanes keep distinct banks)
-    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, close, look) > (size_t)smem_max) nthreads -= 64;
-    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, close, look);
+    const int cq_min = !close ? 0 : (lay == 0 ? kCqMin : kCqMinWide);
+    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, cq_min, look) > (size_t)smem_max) nthreads -= 64;
+    int cq = cq_min;
+    if (const char *ec = getenv("DLS_CLOSE_CQ")) cq = std::max(cq_min, atoi(ec));   // tuning: cap the depth
+    else cq = kCqMax;
+    while (cq > cq_min && smem_bytes(n, vs, prm.L, nthreads, cq, look) > (size_t)smem_max) --cq;
+    if (!close) cq = 0;
+    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, cq, look);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute");
@@ -1593,6 +1703,8 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     if ((e = cudaMemsetAsync(pool, 0, kPoolBytes, stream)) != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(pool)");
     Params q = prm;
     q.pool = (uint32_t *)pool;
+    q.cl_cq = cq;
+    q.one = 1u;
     q.total_warps = (uint32_t)sms * (uint32_t)(nthreads / 32);
     // Cooperative launch: the exit test waits for every warp of the grid to have
     // registered, so all CTAs must be resident at once; the launch guarantees it

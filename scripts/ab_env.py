@@ -18,7 +18,7 @@ sys.path.insert(0, ROOT)
 import paper_1709_02599_b200 as D  # noqa: E402
 import synth  # noqa: E402
 
-KNOBS = ("DLS_CLOSE", "DLS_LOOKAHEAD", "DLS_CLOSE_FORCED", "DLS_MIN_DONATE")
+KNOBS = ("DLS_CLOSE", "DLS_LOOKAHEAD", "DLS_CLOSE_FORCED", "DLS_MIN_DONATE", "DLS_CLOSE_MIN")
 
 
 def run(n, vs, recs, env):

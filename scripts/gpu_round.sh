@@ -1,7 +1,11 @@
-# second GPU call of round 2: smoke, ncu launch list + full capture of the bench kernel, DLS9 A/B
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
-timeout 900 python scripts/ab_env.py --config dls9 --limit 96 --variants "DLS_CLOSE=1;DLS_CLOSE=0;DLS_LOOKAHEAD=51-60;DLS_CLOSE=0,DLS_LOOKAHEAD=51-60" > gpurun_out/ab_dls9.log 2>&1; echo ab_rc=$?
-timeout 600 python scripts/profile_kernel.py --n 8 --launches 1 > gpurun_out/prof_plain.log 2>&1; echo pk_rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:dls_search_kernel -c 1 -o gpurun_out/r2_dls8_close python scripts/profile_kernel.py --n 8 --launches 1 > gpurun_out/ncu_full.log 2>&1; echo ncu_rc=$?
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncul_rc=$?
+P=$PWD/paper_1709_02599_b200
+for i in 1 2; do
+for v in "" _v_v1 _v_nouni; do
+echo "variant libdls_b200$v" >> gpurun_out/ab_step2.log
+DLS_LIB=$P/libdls_b200$v.so timeout 300 python scripts/profile_kernel.py --n 8 --launches 3 >> gpurun_out/ab_step2.log 2>&1
+done
+done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/tests_full.log 2>&1; echo tests_rc=$?
+timeout 900 python scripts/time_configs.py > gpurun_out/time_configs.jsonl 2> gpurun_out/time_configs.err; echo tc_rc=$?
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
