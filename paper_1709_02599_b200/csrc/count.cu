@@ -726,6 +726,7 @@ __device__ __forceinline__ bool load_prefix(const uint8_t *__restrict__ rec, con
 template <int N, bool VS>
 struct Layout {
     static constexpr int NT_FIXED = Geo<N, VS>::LAYOUT < 2 ? 1024 : 0;   // lanes per CTA (0 = runtime)
+    static constexpr int SST_FIXED = NT_FIXED ? NT_FIXED : ((DLS_UNIFIED && Geo<N, VS>::LAYOUT == 3) ? 1024 : 0);
     // a read entry has 2 (byte layout) or 4 words but always a 16-byte lane stride,
     // so the toggle and read parts of a transition share one address register
     static constexpr int BLK_WORDS = 32 * 8;                  // words per transition block
@@ -788,6 +789,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int L = p.L;
     const int NT = LY::NT_FIXED ? LY::NT_FIXED : (int)blockDim.x;
+    // stack slot stride in entries: the lane count, or 1024 for layout 3 (a power
+    // of two lets the unified-address step reach a slot with one multiply-add)
+    const int SST = LY::SST_FIXED ? LY::SST_FIXED : NT;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -795,7 +799,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     char *const stk = reinterpret_cast<char *>(smem + (L + 2) * BLKW);
     // closure event stacks ([slot][lane], Close::EW words per entry) after the
     // stack (16-byte aligned)
-    const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)NT * (uint32_t)sizeof(SW);
+    const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)SST * (uint32_t)sizeof(SW);
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
     const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per slot
     const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
@@ -822,10 +826,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
     }
     // the slots of levels -1 and 0 are read (idle lanes, backtrack from level 1)
     // but never written: they stay 0
-    // slot of level l (l = -1 .. L): S[(l + 1) * NT]
-    SW *const S = reinterpret_cast<SW *>(stk + stack_lane_offset(tid, NT, (int)sizeof(SW)));
+    // slot of level l (l = -1 .. L): S[(l + 1) * SST]
+    SW *const S = reinterpret_cast<SW *>(stk + stack_lane_offset(tid, SST, (int)sizeof(SW)));
     S[0] = 0u;
-    S[NT] = 0u;
+    S[SST] = 0u;
     __syncthreads();
     // transition t: Fl[t * kBlk] (toggle part), Cl at +512 bytes (read part)
     constexpr int kBlk = BLKW / 4;                  // block stride in uint4 units
@@ -991,7 +995,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                     DLS_CHECK(pid >= 0 && (u64)pid < n_prefix && split >= 1 && 2 * split <= L && rest != 0u,
                               kChkPoolGet);
                     for (int l = 1; l < split; ++l)
-                        S[(l + 1) * NT] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
+                        S[(l + 1) * SST] = 1u << ((slot[4 + ((l - 1) >> 3)] >> (4 * ((l - 1) & 7))) & 15u);
                     // consumed: the producer of ticket + kPoolSlots may reuse the slot
                     __threadfence();
                     *const_cast<volatile uint32_t *>(slot + 2) = ticket + 1u;
@@ -1008,7 +1012,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 uint32_t drest = 0;
                 if (pid >= 0 && lvl > 0) {
                     for (int l = 1; l < lvl && l <= L - p.min_donate; ++l) {
-                        const uint32_t s = S[(l + 1) * NT];
+                        const uint32_t s = S[(l + 1) * SST];
                         if (s & (s - 1u)) { dsplit = l; drest = s & (s - 1u); break; }
                     }
                     if (!dsplit && lvl <= L - p.min_donate && (cur & (cur - 1u))) {
@@ -1034,12 +1038,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                         d_pid >= 0), kChkWarpGive);
                     if (recv) {
                         // copy the donor's path above the split level
-                        const SW *const Sd = reinterpret_cast<const SW *>(stk + stack_lane_offset(tid - lane + src, NT, (int)sizeof(SW)));
-                        for (int l = 1; l < d_split; ++l) S[(l + 1) * NT] = Sd[(l + 1) * NT];
+                        const SW *const Sd = reinterpret_cast<const SW *>(stk + stack_lane_offset(tid - lane + src, SST, (int)sizeof(SW)));
+                        for (int l = 1; l < d_split; ++l) S[(l + 1) * SST] = Sd[(l + 1) * SST];
                     }
                     __syncwarp();
                     if (give) {
-                        if (dsplit < lvl) S[(dsplit + 1) * NT] &= 0u - S[(dsplit + 1) * NT];
+                        if (dsplit < lvl) S[(dsplit + 1) * SST] &= 0u - S[(dsplit + 1) * SST];
                         else cur &= 0u - cur;
                         dsplit = 0;
                     }
@@ -1082,13 +1086,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
                                 uint32_t word = 0;
                                 for (int k = 0; k < 8; ++k) {
                                     const int l = 1 + w * 8 + k;
-                                    if (l < dsplit) word |= (uint32_t)(__ffs(S[(l + 1) * NT]) - 1) << (4 * k);
+                                    if (l < dsplit) word |= (uint32_t)(__ffs(S[(l + 1) * SST]) - 1) << (4 * k);
                                 }
                                 slot[4 + w] = word;
                             }
                             __threadfence();
                             *(volatile uint32_t *)slot = ticket + 1u;
-                            if (dsplit < lvl) S[(dsplit + 1) * NT] &= 0u - S[(dsplit + 1) * NT];
+                            if (dsplit < lvl) S[(dsplit + 1) * SST] &= 0u - S[(dsplit + 1) * SST];
                             else cur &= 0u - cur;
                             atomicAdd(acc + 2, 1ull);
                         }
@@ -1117,9 +1121,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             } else {                           // a donated subtree
                 for (int l = 1; l < split; ++l) {
                     if constexpr (Geo<N, VS>::LAYOUT >= 3)
-                        st.toggle(Fl[l * kBlk], Cl[l * kBlk], S[(l + 1) * NT], 0u);
+                        st.toggle(Fl[l * kBlk], Cl[l * kBlk], S[(l + 1) * SST], 0u);
                     else
-                        st.toggle(Fl[l * kBlk], S[(l + 1) * NT], 0u);
+                        st.toggle(Fl[l * kBlk], S[(l + 1) * SST], 0u);
                 }
                 lvl = split;
                 cur = rest;
@@ -1228,7 +1232,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const bool dn = cur != 0u;                     // descend: cell(lvl) has candidates
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
             const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
-            SW *const sl = S + lvl * NT;                   // slot of level lvl-1
+            SW *const sl = S + lvl * SST;                   // slot of level lvl-1
             const uint32_t sp = *sl;                       // its L (lowest bit = assigned value)
             const uint32_t bb = sp & (0u - sp);
             const uint32_t sibs = sp - bb;                 // L &= L-1
@@ -1236,7 +1240,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const bool mv = !dn && sibs != 0u;             // advance: re-assign level lvl-1
             DLS_CHECK(lvl >= 0 && lvl <= L + 1 && (!dn || lvl <= L) && (lvl > 0 || (!dn && !mv)), kChkStep);
             if constexpr (!DLS_ONE_STORE) {
-                if (dn) sl[NT] = cur;                      // push L of level lvl
+                if (dn) sl[SST] = cur;                      // push L of level lvl
                 if (mv) sl[0] = sibs;
             }
             const int toff = t * (BLKW * 4);     // byte offset of transition t
@@ -1265,10 +1269,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if constexpr (DLS_ONE_STORE) {
                 // the slot a push (slot lvl+1) or an advance (slot lvl) writes is
                 // slot nl in both cases: the address the next step loads from
-                if (adv) S[nl * NT] = (SW)(dn ? cur : sibs);
+                if (adv) S[nl * SST] = (SW)(dn ? cur : sibs);
             }
             if (!CLOSE) cnt32 += nl > L ? 1u : 0u;    // (CLOSE: the closure rounds add to cnt32)
-            if (EMIT && nl > L) emit_square<N, VS, SW>(p, pid, S, NT);
+            if (EMIT && nl > L) emit_square<N, VS, SW>(p, pid, S, SST);
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
             lvl = nl;
@@ -1313,7 +1317,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         if (lane == 0) acc[1] += (u64)wn;
     }
 
-    DLS_CHECK(lvl == 0 && pid < 0 && cnt == 0u && cur == 0u && S[0] == 0u && S[NT] == 0u, kChkExit);
+    DLS_CHECK(lvl == 0 && pid < 0 && cnt == 0u && cur == 0u && S[0] == 0u && S[SST] == 0u, kChkExit);
     // ------------------------------------------------ block reduction, 1 atomic per block
     __syncthreads();
     if (tid == 0) {
