@@ -57,6 +57,11 @@ OPS_PER_NODE = 12
 # 30; final test and shift (3) -> 87
 OPS_PER_CLOSURE = 87
 DLS8_COUNT = 7447587840
+# nodes of the full Alg. 4 tree below the 547 896 workunits (every one of the 42
+# cells assigned one by one, as the paper's loop nest does): the plain search
+# (DLS_CLOSE=0) reports it, profiles/r2_ab_step.log; node parity with the oracle
+# on sampled workunits: tests/test_gpu_parity.py
+DLS8_ALG4_TREE_NODES = 368133443872
 PAPER_CONTEXT = "paper: 5.8e6 DLS8 squares/s on one core of an Intel Core i7-6770 (Table 1, P:281); context only"
 
 
@@ -370,9 +375,16 @@ def main():
                                                       "capture (profiles/%s) = the 35 MB of workunit records: "
                                                       "the search itself never touches HBM" % NCU_JSON),
                          "ops_per_node": OPS_PER_NODE, "ops_per_closure": OPS_PER_CLOSURE,
+                         # context: the same time against the work of the paper's own loop
+                         # nest (its full tree, 12 ops per node) -- what the closure saves
+                         # shows up here, not in frac
+                         "frac_of_peak_alg4_full_tree": (DLS8_ALG4_TREE_NODES * OPS_PER_NODE / world
+                                                         / (per_launch_ms / 1e3) / 1e12) / peak,
+                         "alu_pipe_busy_ncu": (ncu.get("alu_pipe_pct", 0) / 100.0) if ncu else None,
+                         "fmaheavy_pipe_busy_ncu": (ncu.get("fmaheavy_pipe_pct", 0) / 100.0) if ncu else None,
                          "issue_slots_busy_ncu": (ncu.get("issue_slots_busy_pct", 0) / 100.0) if ncu else None,
-                         # the unit that binds the kernel: the shared-memory data pipe
-                         # (table + stack loads), not the integer issue rate
+                         # issue slots, ALU pipe, FMA-heavy pipe and the shared-memory
+                         # data pipe are all 70-90% busy
                          "smem_pipe_busy_ncu": (ncu.get("smem_lsu_wavefronts_pct", 0) / 100.0) if ncu else None,
                          "note": "integer-issue roofline at %.0f MHz (MEASURED_PEAKS sm_max_mhz): 148 SMs x 4 SMSP x "
                                  "32 lanes; achieved = (%d int ops x nodes the kernel visits (Alg. 4 loop body) + "

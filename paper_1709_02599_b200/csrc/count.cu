@@ -95,6 +95,11 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_STEP_V2
 #define DLS_STEP_V2 1
 #endif
+// DLS_STEP_V3=1 (needs V2): the stack slot is loaded only by lanes that do not
+// descend (0 otherwise), which makes two more selects of the step plain ORs / subtractions
+#ifndef DLS_STEP_V3
+#define DLS_STEP_V3 0
+#endif
 // A closure round (every lane evaluates its newest event) starts once this many
 // lanes of the warp hold one (A/B: profiles/r2_ab_close_min.log)
 constexpr int kCloseMinLanes = 24;
@@ -162,6 +167,9 @@ struct Params {
     uint32_t cl_open;        // tracked columns with empty cells in rows r1, r2
     int cl_E;                // popc(cl_open)
     int cl_rword;            // mask-layout word holding row r1's field
+    // layouts 3, 4: rows cl_swap_a and cl_swap_b trade their fields (-1: none), so
+    // that row r1 always sits in word R[2] and the event store needs no select
+    int cl_swap_a, cl_swap_b;
     int cl_rshift;           // bit offset of row r1's field in that word
     uint32_t cl_sel[10];     // field selectors of the columns of J (padded)
     int cl_min;              // lanes of a warp holding an event that start an evaluation round
@@ -378,6 +386,15 @@ struct Masks<N, VS, 3> {
     __device__ __forceinline__ void toggle(const uint4 &f, const uint4 &g, uint32_t bnew, uint32_t bold) {
         toggle_d(f, g, bnew - bold);
     }
+    // rows a and b trade their fields (once per adopted record)
+    __device__ __forceinline__ void swap_rows(int a, int b) {
+        const int sa = (a % FPW) * N, sb = (b % FPW) * N;
+        const uint32_t wa = a / FPW == 0 ? R[0] : (a / FPW == 1 ? R[1] : R[2]);
+        const uint32_t wb = b / FPW == 0 ? R[0] : (b / FPW == 1 ? R[1] : R[2]);
+        const uint32_t x = ((wa >> sa) ^ (wb >> sb)) & G::ALLN;
+#pragma unroll
+        for (int w = 0; w < 3; ++w) R[w] ^= (a / FPW == w ? x << sa : 0u) ^ (b / FPW == w ? x << sb : 0u);
+    }
     __device__ __forceinline__ static uint32_t pick(const uint32_t (&a)[3], uint32_t sel) {
         const uint32_t w = (sel & 64u) ? a[2] : ((sel & 32u) ? a[1] : a[0]);
         return __funnelshift_r(w, 0u, sel);          // shift by sel & 31
@@ -420,6 +437,16 @@ struct Masks<N, VS, 4> {
     }
     __device__ __forceinline__ void toggle(const uint4 &f, const uint4 &g, uint32_t bnew, uint32_t bold) {
         toggle_d(f, g, bnew - bold);
+    }
+    // rows a, b >= 1 trade their fields (once per adopted record)
+    __device__ __forceinline__ void swap_rows(int a, int b) {
+        const int ia = a - 1, ib = b - 1;
+        const int sa = (ia % 3) * N, sb = (ib % 3) * N;
+        const uint32_t wa = ia / 3 == 0 ? R[0] : (ia / 3 == 1 ? R[1] : R[2]);
+        const uint32_t wb = ib / 3 == 0 ? R[0] : (ib / 3 == 1 ? R[1] : R[2]);
+        const uint32_t x = ((wa >> sa) ^ (wb >> sb)) & G::ALLN;
+#pragma unroll
+        for (int w = 0; w < 3; ++w) R[w] ^= (ia / 3 == w ? x << sa : 0u) ^ (ib / 3 == w ? x << sb : 0u);
     }
     __device__ __forceinline__ static uint32_t pick(const uint32_t (&a)[3], uint32_t x, uint32_t sel) {
         const uint32_t w = (sel & 64u) ? ((sel & 32u) ? x : a[2]) : ((sel & 32u) ? a[1] : a[0]);
@@ -561,9 +588,9 @@ template <int N, bool VS>
 struct Close<N, VS, 3> : CloseBase<N, VS> {
     typedef CloseBase<N, VS> B;
     static constexpr int EW = 4;
-    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t rsel) {
-        const uint32_t rw = rsel == 2 ? st.R[2] : (rsel == 1 ? st.R[1] : st.R[0]);
-        return make_uint4(st.C[0], st.C[1], st.C[2], rw);
+    // (the host moves row r1 into word R[2]: cl_swap_a / cl_swap_b, cl_rword = 2)
+    __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t) {
+        return make_uint4(st.C[0], st.C[1], st.C[2], st.R[2]);
     }
     __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
         uint4 w = *reinterpret_cast<const uint4 *>(src);
@@ -601,9 +628,8 @@ struct Close<N, VS, 4> : CloseBase<N, VS> {
     __device__ __forceinline__ static uint4 pack(const Masks<N, VS> &st, uint32_t) {
         return make_uint4(st.C[0], st.C[1], st.C[2], st.X);
     }
-    __device__ __forceinline__ static uint32_t pack_row(const Masks<N, VS> &st, uint32_t rsel) {
-        return rsel == 3 ? st.X : (rsel == 2 ? st.R[2] : (rsel == 1 ? st.R[1] : st.R[0]));
-    }
+    // (the host moves row r1 into word R[2]: cl_swap_a / cl_swap_b, cl_rword = 2)
+    __device__ __forceinline__ static uint32_t pack_row(const Masks<N, VS> &st, uint32_t) { return st.R[2]; }
     __device__ __forceinline__ static uint32_t eval(const uint32_t *src, const Params &p, uint32_t rsel) {
         uint4 w = *reinterpret_cast<const uint4 *>(src);
         uint32_t rw = src[4];
@@ -841,11 +867,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // unified-address step (DLS_UNIFIED): shared addresses of the lane's entry of
     // transition 0 and of level L + 1, and the distance from a level's entry to
     // the stack slot S[level * NT]
-    constexpr bool kUni = DLS_UNIFIED && Geo<N, VS>::LAYOUT == 0 && !LOOK && !EMIT && BLKW * 4 == 1024 &&
-                          LY::NT_FIXED == 1024 && sizeof(SW) == 1;
+    constexpr bool kUni = DLS_UNIFIED && (Geo<N, VS>::LAYOUT == 0 || Geo<N, VS>::LAYOUT == 1 || Geo<N, VS>::LAYOUT == 3) &&
+                          !LOOK && !EMIT && BLKW * 4 == 1024 && LY::SST_FIXED == 1024;
+    constexpr int kSS = sizeof(SW) == 1 ? 0 : 1;     // a stack slot is 1024 << kSS bytes
     const uint32_t fl_sa = (uint32_t)__cvta_generic_to_shared(Fb);
     const uint32_t x_last = fl_sa + ((uint32_t)L << 10);          // above it: level L + 1
-    const uint32_t d_stk = (uint32_t)__cvta_generic_to_shared(S) - fl_sa;
+    const uint32_t d_stk = (uint32_t)__cvta_generic_to_shared(S) - (fl_sa << kSS);   // slot = (entry << kSS) + d_stk
     const uint32_t d_rd = (uint32_t)__cvta_generic_to_shared(Cb) - fl_sa;   // entry -> its read part
     // (LOOK) watched-cell entries: 8-byte lane stride after the 1024 bytes of the two parts
     const char *const Lb = reinterpret_cast<const char *>(smem + BLKW + 256) + 8 * lane;
@@ -1104,6 +1131,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             DLS_CHECK(pid >= 0 && (u64)pid < n_prefix && split >= 0 && split <= L, kChkAdopt);
             // rebuild Rows/Columns from the record, then replay the path
             const bool ok = load_prefix<N, VS>(p.prefixes + (u64)pid * (u64)(N * N), p.pat[0], p.pat[1], st);
+            if constexpr (CLOSE && Geo<N, VS>::LAYOUT >= 3) {
+                if (p.cl_swap_a >= 0) st.swap_rows(p.cl_swap_a, p.cl_swap_b);
+            }
             cnt = 0;
             if (split == 0) {                  // a fresh workunit from the queue
                 if (!ok) {
@@ -1148,14 +1178,27 @@ dls_search_kernel(const __grid_constant__ Params p) {
         for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
             const bool dn = cur != 0u;
             uint32_t sp;                                   // L of level lvl-1
-            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(one * d_stk + xq));
+#if DLS_STEP_V3
+            // loaded only when the step does not descend (else 0: then bb = sibs = 0)
+            if constexpr (kSS == 0)
+                asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.shared.u8 %0, [%1];\n\t}"
+                             : "=&r"(sp) : "r"(one * d_stk + xq), "r"(cur));
+            else
+                asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.shared.u16 %0, [%1];\n\t}"
+                             : "=&r"(sp) : "r"((xq << kSS) + d_stk), "r"(cur));
+#else
+            if constexpr (kSS == 0)
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(one * d_stk + xq));
+            else
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(sp) : "r"((xq << kSS) + d_stk));
+#endif
             const uint32_t bb = sp & (0u - sp);            // its lowest bit: the value assigned there
             const uint32_t sibs = sp - bb;                 // L &= L-1
 #if DLS_STEP_V2
             // the level this step (re)assigns holds X: level lvl's candidates on a
             // descend, the untried siblings of level lvl-1 otherwise; empty =
             // plain backtrack.  One select, one lowest-bit isolation.
-            const uint32_t X = dn ? cur : sibs;
+            const uint32_t X = DLS_STEP_V3 ? (cur | sibs) : (dn ? cur : sibs);
             const bool adv = X != 0u;
             const uint32_t x = X & (0u - X);
             DLS_CHECK(xq >= fl_sa && xq <= fl_sa + ((uint32_t)(L + 1) << 10) && (!dn || xq <= fl_sa + ((uint32_t)L << 10)) &&
@@ -1173,18 +1216,24 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const uint32_t xt = dn ? xq : addk(xq, 0u - 1024u);   // transition t = dn ? lvl : lvl - 1
 #endif
             uint4 f;
-            uint2 cs;
+            CT cs;
             asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(f.x), "=r"(f.y), "=r"(f.z), "=r"(f.w) : "r"(xt));
-            if constexpr (kRead8)
+            if constexpr (sizeof(CT) == 16)
+                asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+512];" : "=r"(cs.x), "=r"(cs.y), "=r"(cs.z), "=r"(cs.w) : "r"(xt));
+            else if constexpr (kRead8)
                 asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(cs.x), "=r"(cs.y) : "r"(one * d_rd + xt));
             else
                 asm("ld.shared.v2.u32 {%0, %1}, [%2+512];" : "=r"(cs.x), "=r"(cs.y) : "r"(xt));
 #if DLS_STEP_V2
-            if constexpr (VS) {
-                st.toggle(f, x, dn ? 0u : bb);             // mark / unmark
+            if constexpr (Geo<N, VS>::LAYOUT == 3) {
+                uint32_t d = x;
+                if (DLS_STEP_V3 || !dn) d = x - bb;
+                st.toggle_d(f, cs, d);                     // mark / unmark
+            } else if constexpr (VS) {
+                st.toggle(f, x, (DLS_STEP_V3 || !dn) ? bb : 0u);
             } else {
                 uint32_t d = x;
-                if (!dn) d = x - bb;
+                if (DLS_STEP_V3 || !dn) d = x - bb;
                 st.toggle_d(f, d, d);
             }
             const uint32_t c = st.cand(cs);
@@ -1192,7 +1241,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if (adv) xn = addk(xt, 1024u);
             xn = max(xn, fl_sa);
 #else
-            if constexpr (VS) {
+            if constexpr (Geo<N, VS>::LAYOUT == 3) {
+                st.toggle_d(f, cs, dn ? b : sb - bb);
+            } else if constexpr (VS) {
                 st.toggle(f, dn ? b : sb, dn ? 0u : bb);
             } else {
                 const uint32_t d = dn ? b : sb - bb;
@@ -1201,7 +1252,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const uint32_t c = st.cand(cs);
             const uint32_t xn = max(adv ? addk(xt, 1024u) : xt, fl_sa);   // level nl = max(t + adv, 0)
 #endif
-            if (adv) asm volatile("st.shared.u8 [%0], %1;" :: "r"(one * d_stk + xn), "r"(X));
+            if constexpr (kSS == 0) {
+                if (adv) asm volatile("st.shared.u8 [%0], %1;" :: "r"(one * d_stk + xn), "r"(X));
+            } else {
+                if (adv) asm volatile("st.shared.u16 [%0], %1;" :: "r"((xn << kSS) + d_stk), "r"(X));
+            }
             if (!CLOSE) cnt32 += xn > x_last ? 1u : 0u;
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
@@ -1380,7 +1435,9 @@ int layout_of(int n, bool vs) {
          : (n == 10 && !vs && DLS_LAYOUT10 == 4) ? 4 : 2;
 }
 
-void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
+// swap_a / swap_b (layouts 3, 4; -1: none): these two rows trade their fields
+// (Params::cl_swap_a).
+void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab, int swap_a = -1, int swap_b = -1) {
     const int L = (int)level_cells.size();
     const int lay = layout_of(n, vs);
     const bool bytes = lay == 0;
@@ -1389,11 +1446,12 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
     const int rpw = 64 / rf, cpw = 64 / cf;
     const int rpw32 = 32 / rf, cpw32 = 32 / cf;
     auto cell_of = [&](int l) { return level_cells[l - 1]; };   // level l = 1..L
+    auto slot = [&](int i) { return (lay == 3 || lay == 4) ? (i == swap_a ? swap_b : (i == swap_b ? swap_a : i)) : i; };
     for (int t = -1; t <= L; ++t) {
         Tab &e = tab[t + 1];
         std::memset(&e, 0, sizeof(e));
         if (t >= 1) {                       // toggle part: cell(t)
-            const int i = cell_of(t) / n, j = cell_of(t) % n;
+            const int i = slot(cell_of(t) / n), j = cell_of(t) % n;
             if (bytes) {
                 (i < 4 ? e.w[0] : e.w[1]) = 1u << (8 * (i & 3));
                 (j < 4 ? e.w[2] : e.w[3]) = 1u << (8 * (j & 3));
@@ -1419,7 +1477,7 @@ void fill_tab(int n, bool vs, const std::vector<int> &level_cells, Tab *tab) {
             // level L+1 reads row 0 (assigned in every record, hence full), so its
             // candidate set is empty
             const int cl = std::min(t + 1, L);
-            const int i = t + 1 > L ? 0 : cell_of(cl) / n, j = cell_of(cl) % n;
+            const int i = t + 1 > L ? 0 : slot(cell_of(cl) / n), j = cell_of(cl) % n;
             if (bytes) {
                 e.w[4] = (uint32_t)i;
                 e.w[5] = (uint32_t)j;
@@ -1496,12 +1554,23 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
         if (l == 0) return -1;       // already closable at the records: plain search
         const int h = n / 2, rf = vs ? (h > 0 ? h : 1) : n, rpw32 = 32 / rf, cpw32 = 32 / n;
         // row r1's word in the mask layout (the closure reads row r1 from it)
-        int rword = 0;
+        // (layouts 3, 4: row r1 trades places with a row of word R[2], so the step's
+        // event store always takes R[2]; a row slot below is the row's place after that)
+        int rword = 0, swap_a = -1, swap_b = -1;
+        if (lay == 3 || lay == 4) {
+            if (r1 == 0) return -1;                          // (row 0 is assigned in every record)
+            const int first = lay == 3 ? 6 : 7;              // rows of word R[2]: first .. first + 2
+            if (r1 < first) {
+                swap_a = r1;
+                swap_b = first == r2 ? first + 1 : first;
+            }
+        }
+        auto slot = [&](int i) { return i == swap_a ? swap_b : (i == swap_b ? swap_a : i); };
+        const int s1 = slot(r1);                              // row r1's place
         switch (lay) {
             case 0: rword = r1 >= 4; break;
             case 1: rword = r1 / rpw32; break;
-            case 3: rword = r1 / 3; break;
-            default: rword = r1 == 0 ? 3 : (r1 - 1) / 3;
+            default: rword = 2;
         }
         // walk back over forced cells just before level l (up to 2): the closure
         // assigns them itself.  A cell qualifies if its row or column has every
@@ -1526,7 +1595,7 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
                 const int cell = plan.cells[depth + l - 1];
                 const int i = cell / n, j = cell % n;
                 if (i == r1 || i == r2) break;
-                if ((lay == 3 || lay == 4) && (lay == 3 ? i / 3 : (i == 0 ? 3 : (i - 1) / 3)) != rword) break;
+                if ((lay == 3 || lay == 4) && (lay == 3 ? slot(i) / 3 : (i == 0 ? 3 : (slot(i) - 1) / 3)) != rword) break;
                 int rowc = 0, colc = 0;
                 for (int k = 0; k < n; ++k) {
                     if (k != j && assigned_before(l, i * n + k)) ++rowc;
@@ -1556,6 +1625,8 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
             if (open >> j & 1u) prm->cl_sel[k++] = sel(j);
         while (k < 10) prm->cl_sel[k++] = sel(pad);
         prm->close = 1;
+        prm->cl_swap_a = swap_a;
+        prm->cl_swap_b = swap_b;
         prm->cl_min = kCloseMinLanes;
         if (const char *e = getenv("DLS_CLOSE_MIN")) prm->cl_min = std::min(32, std::max(1, atoi(e)));   // tuning
         prm->cl_open = open;
@@ -1563,17 +1634,15 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
         prm->cl_nf = nf;
         for (int k = 0; k < nf; ++k) {      // apply in plan order: the earlier cell first
             Tab t3[3];
-            fill_tab(n, vs, std::vector<int>{fcell[nf - 1 - k]}, t3);
+            fill_tab(n, vs, std::vector<int>{fcell[nf - 1 - k]}, t3, swap_a, swap_b);
             prm->cl_fread[k] = t3[1];       // transition 0 reads cell(1)
             prm->cl_ftog[k] = t3[2];        // transition 1 toggles cell(1)
         }
         switch (lay) {
             case 0: prm->cl_rword = r1 >= 4; prm->cl_rshift = 8 * (r1 & 3); break;
             case 1: prm->cl_rword = r1 / rpw32; prm->cl_rshift = (r1 % rpw32) * rf; break;
-            case 3: prm->cl_rword = r1 / 3; prm->cl_rshift = n * (r1 % 3); break;
-            default:
-                if (r1 == 0) { prm->cl_rword = 3; prm->cl_rshift = n; }
-                else { prm->cl_rword = (r1 - 1) / 3; prm->cl_rshift = n * ((r1 - 1) % 3); }
+            case 3: prm->cl_rword = 2; prm->cl_rshift = n * (s1 % 3); break;
+            default: prm->cl_rword = 2; prm->cl_rshift = n * ((s1 - 1) % 3);
         }
         return l;
     }
@@ -1599,13 +1668,14 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm, bool allow_close
         return DLS_E_ARG;
     }
     std::memset(prm, 0, sizeof(*prm));
+    prm->cl_swap_a = prm->cl_swap_b = -1;
     prm->L = steps - depth;
     if (allow_close) {
         const int lc = closure_level(plan, depth, prm);
         if (lc >= 0) prm->L = lc;
     }
     std::vector<int> level_cells(plan.cells.begin() + depth, plan.cells.begin() + depth + prm->L);
-    fill_tab(n, symmetric, level_cells, prm->tab);
+    fill_tab(n, symmetric, level_cells, prm->tab, prm->cl_swap_a, prm->cl_swap_b);
     // lookahead, DLS N = 9 only, opt-in: DLS_LOOKAHEAD=a-b applies it
     // after the plan steps a..b (1-based, Fig. 1 numbering; the paper: 51-60).
     // The watched cell of a step assigning (i, j) is the first later plan cell
@@ -1624,7 +1694,7 @@ int prepare_plan(const dls::Plan &plan, int depth, Params *prm, bool allow_close
                     const int c = plan.cells[q];
                     if (c / n != i0 && c % n != j0) continue;
                     Tab t3[3];
-                    fill_tab(n, symmetric, std::vector<int>{c}, t3);
+                    fill_tab(n, symmetric, std::vector<int>{c}, t3, prm->cl_swap_a, prm->cl_swap_b);
                     prm->look_sel[t + 1][0] = t3[1].w[6];
                     prm->look_sel[t + 1][1] = t3[1].w[7];
                     break;
@@ -1666,7 +1736,8 @@ constexpr int kCqMin = 8, kCqMinWide = 6, kCqMax = 16;
 size_t smem_bytes(int n, bool vs, int L, int nthreads, int cq, bool look = false) {
     const int lay = layout_of(n, vs);
     const size_t sw = lay == 0 ? 1 : 2;                       // Layout::SW
-    const size_t stack = (size_t)(L + 1 + 4 / sw) * nthreads * sw;
+    const size_t sst = (lay == 3 && DLS_UNIFIED) ? 1024 : nthreads;   // Layout::SST_FIXED
+    const size_t stack = (size_t)(L + 1 + 4 / sw) * sst * sw;
     const size_t base = (size_t)(L + 2) * (look ? 40 : 32) * 32 + ((stack + 15) & ~(size_t)15);
     const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
     return base + (size_t)cq * nthreads * ew * 4;             // event stacks

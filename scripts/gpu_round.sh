@@ -1,11 +1,7 @@
 mkdir -p gpurun_out
 P=$PWD/paper_1709_02599_b200
-for i in 1 2; do
-for v in "" _v_v1 _v_nouni; do
-echo "variant libdls_b200$v" >> gpurun_out/ab_step2.log
-DLS_LIB=$P/libdls_b200$v.so timeout 300 python scripts/profile_kernel.py --n 8 --launches 3 >> gpurun_out/ab_step2.log 2>&1
-done
-done
+timeout 900 python scripts/ab_env.py --config dls9 --limit 64 --variants "DLS_CLOSE=1;DLS_CLOSE=0" > gpurun_out/ab_dls9_uni.log 2>&1; echo ab9_rc=$?
+DLS_LIB=$P/libdls_b200_v_nouni.so timeout 900 python scripts/ab_env.py --config dls9 --limit 64 --variants "DLS_CLOSE=1;DLS_CLOSE=0" > gpurun_out/ab_dls9_nouni.log 2>&1
+timeout 900 python scripts/ab_env.py --config vs10 --limit 256 --variants "DLS_CLOSE=1;DLS_CLOSE=0" > gpurun_out/ab_vs10_uni.log 2>&1; echo ab10_rc=$?
+DLS_LIB=$P/libdls_b200_v_nouni.so timeout 900 python scripts/ab_env.py --config vs10 --limit 256 --variants "DLS_CLOSE=1" > gpurun_out/ab_vs10_nouni.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/tests_full.log 2>&1; echo tests_rc=$?
-timeout 900 python scripts/time_configs.py > gpurun_out/time_configs.jsonl 2> gpurun_out/time_configs.err; echo tc_rc=$?
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?

@@ -46,6 +46,7 @@ def main():
         "issue_slots_busy_pct": num(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "alu_pipe_pct": num(d, "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
         "fma_pipe_pct": num(d, "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+        "fmaheavy_pipe_pct": num(d, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "smem_lsu_wavefronts_pct": num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
         "smem_wavefronts": int(num(d, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")),
         "smem_bank_conflicts": int(num(d, "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")),

@@ -27,8 +27,14 @@ def _pre(n, fixed):
     return pre
 
 
-def _word(n, i):
-    """Mask word of row i in the kernel's layouts 3 (n = 9) / 4 (n = 10)."""
+def _word(n, i, r1=None, r2=None):
+    """Mask word of row i in the kernel's layouts 3 (n = 9) / 4 (n = 10).  With a
+    closure, row r1 trades places with the first row of word 2 other than r2
+    (unless r1 is in word 2 already), so that the event store always takes word 2."""
+    first = 6 if n == 9 else 7
+    if r1 is not None and r1 < first:
+        b = first + 1 if first == r2 else first
+        i = b if i == r1 else (r1 if i == b else i)
     return i // 3 if n == 9 else (3 if i == 0 else (i - 1) // 3)
 
 
@@ -67,7 +73,7 @@ def closure_level(n, vs, order, depth, fixed=True, walk=False):
         forced = []
         while walk and len(forced) < 2 and l - 1 >= 1 and not vs:
             i, j = divmod(order[depth + l - 1], n)
-            if i in (r1, r2) or (n >= 9 and _word(n, i) != _word(n, r1)):
+            if i in (r1, r2) or (n >= 9 and _word(n, i, r1, r2) != _word(n, r1, r1, r2)):
                 break
             before = np.ones((n, n), bool)          # still empty before level l
             before[pre == 1] = False
