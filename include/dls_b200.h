@@ -238,6 +238,33 @@ int dls_random_prefix(int n, int symmetric, const uint8_t *record, const int32_t
                       int n_cells, uint64_t seed, uint8_t *out_record, double *out_weight);
 
 /*
+ * dls_scale_total -- the full count from the first-row-fixed count (row 0
+ * is fixed "in all algorithms and experiments"; N! x the fixed count).
+ * The multiplier is N! for DLS and (N/2)! * 2^(N/2) for vertically symmetric DLS
+ * (a renaming keeps the symmetry only if it commutes with x -> N-1-x; DESIGN.md
+ * R3); 0 for odd N with symmetric = 1.
+ *   count_fixed     the count with row 0 = 0..N-1
+ *   out128          host, 2 words or NULL: count_fixed * multiplier, low word first
+ *   out_multiplier  host or NULL
+ * Host arithmetic only (no device needed).  Returns DLS_OK or DLS_E_ARG.
+ */
+int dls_scale_total(int n, int symmetric, uint64_t count_fixed, uint64_t *out128, uint64_t *out_multiplier);
+
+/*
+ * dls_mc_estimate -- the Monte Carlo estimate of Section 5.3 from
+ * n_samples Knuth descents (dls_random_prefix: weight w_s, completions c_s
+ * counted by dls_count_cells):
+ *   out[0] = mean of w_s * c_s        (unbiased estimate of the count)
+ *   out[1] = its standard error       (sample standard deviation / sqrt(n); NaN for n < 2)
+ *   out[2] = n_k * sum(w c) / sum(w)  (the paper's "N^k x mean completions" form;
+ *                                      n_k = number of consistent k-cell prefixes)
+ *   out[3] = sum(w c) / sum(w)        (weighted mean completions per prefix)
+ * weights, counts: host arrays of n_samples; out: host, 4 doubles.
+ * Host arithmetic only.  Returns DLS_OK or DLS_E_ARG.
+ */
+int dls_mc_estimate(const double *weights, const uint64_t *counts, int64_t n_samples, double n_k, double *out);
+
+/*
  * dls_kernel_launches -- number of kernels dls_count / dls_count_async enqueue
  * per call (for the bench's launch count): the search kernel only.
  */

@@ -7,7 +7,8 @@ include/dls_b200.h; this package is its thin binding plus convenience wrappers.
 """
 from ._binding import (DLS_EMPTY, DLS_MAX_ORDER, DLS_STATS_WORDS, DlsError, dls_canonize, dls_count,  # noqa: F401
                        dls_count_async, dls_count_cells, dls_count_sb, dls_count_sb_range, dls_emit, dls_random_prefix,
-                       dls_kernel_launches, dls_plan, dls_refine, dls_search_levels, dls_split,
+                       dls_kernel_launches, dls_mc_estimate, dls_plan, dls_refine, dls_scale_total, dls_search_levels,
+                       dls_split,
                        dls_version,
                        lib_path, load)
 from .api import count_squares, default_split_depth, count_prefixes  # noqa: F401

@@ -16,7 +16,7 @@ import time
 import numpy as np
 
 from . import _binding as B
-from .api import count_squares, first_row_multiplier
+from .api import count_squares
 
 
 def cmd_plan(a):
@@ -41,7 +41,7 @@ def cmd_count(a):
         r = count_squares(a.n, a.vs, not a.free)
     r["seconds"] = time.perf_counter() - t
     if not a.free:
-        r["total_all_first_rows"] = r["count"] * first_row_multiplier(a.n, a.vs)
+        r["total_all_first_rows"] = B.dls_scale_total(a.n, r["count"], a.vs)[0]
     print(json.dumps(r))
 
 
@@ -57,17 +57,18 @@ def cmd_estimate(a):
     rec = np.full((a.n, a.n), 255, np.uint8)
     rec[0, :] = np.arange(a.n)
     cells = list(range(a.n, a.k))
-    vals = []
+    ws, cs = [], []
     for s in range(a.samples):
         pre, w = B.dls_random_prefix(a.n, rec, cells, a.seed * 1000003 + s, a.vs)
         c = 0
         if w > 0:
             rest = [i for i in range(a.n * a.n) if pre.reshape(-1)[i] == 255 and (not a.vs or 2 * (i % a.n) <= a.n - 1)]
             c, _ = B.dls_count_cells(a.n, pre, rest, a.vs)
-        vals.append(w * c)
-    v = np.array(vals, dtype=np.float64)
-    print(json.dumps({"n": a.n, "k": a.k, "samples": a.samples, "estimate": v.mean(),
-                      "stderr": v.std(ddof=1) / math.sqrt(len(v)) if len(v) > 1 else None}))
+        ws.append(w)
+        cs.append(c)
+    est = B.dls_mc_estimate(ws, cs, 0.0)
+    print(json.dumps({"n": a.n, "k": a.k, "samples": a.samples, "estimate": est["knuth"],
+                      "stderr": None if a.samples < 2 else est["knuth_se"]}))
 
 
 def main(argv=None):

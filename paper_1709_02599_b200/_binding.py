@@ -21,7 +21,7 @@ DLS_OK, DLS_E_ARG, DLS_E_CUDA, DLS_E_PREFIX, DLS_E_NODEVICE = 0, -1, -2, -3, -4
 
 EXPORTS = ("dls_version", "dls_last_error", "dls_plan", "dls_split", "dls_refine", "dls_emit", "dls_count",
            "dls_count_async", "dls_canonize", "dls_count_sb", "dls_count_sb_range", "dls_count_cells",
-           "dls_random_prefix", "dls_kernel_launches", "dls_search_levels")
+           "dls_random_prefix", "dls_kernel_launches", "dls_search_levels", "dls_scale_total", "dls_mc_estimate")
 
 _lib = None
 
@@ -75,6 +75,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
     lib.dls_kernel_launches.restype = c_int
     lib.dls_search_levels.argtypes = [c_int, c_int, c_int, c_int, vp]
     lib.dls_search_levels.restype = c_int
+    lib.dls_scale_total.argtypes = [c_int, c_int, ctypes.c_uint64, vp, vp]
+    lib.dls_scale_total.restype = c_int
+    lib.dls_mc_estimate.argtypes = [vp, vp, c_i64, ctypes.c_double, vp]
+    lib.dls_mc_estimate.restype = c_int
     _lib = lib
     return lib
 
@@ -283,3 +287,26 @@ def dls_search_levels(n: int, depth: int, symmetric: bool = False, fixed_first_r
 
 def dls_kernel_launches() -> int:
     return int(load().dls_kernel_launches())
+
+
+def dls_scale_total(n: int, count_fixed: int, symmetric: bool = False):
+    """-> (count_fixed * multiplier, multiplier): the full count from the first-row-fixed
+    one (R3 for vertical symmetry).  128-bit product formed in the library."""
+    out = (ctypes.c_uint64 * 2)()
+    m = ctypes.c_uint64(0)
+    _check(load().dls_scale_total(n, int(symmetric), ctypes.c_uint64(int(count_fixed)), ctypes.addressof(out),
+                                  ctypes.addressof(m)), "dls_scale_total")
+    return int(out[0]) | (int(out[1]) << 64), int(m.value)
+
+
+def dls_mc_estimate(weights, counts, n_k: float):
+    """Section 5.3 estimate from Knuth samples -> dict(knuth, knuth_se, ratio, mean_completions_weighted)."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    if w.shape != c.shape or w.ndim != 1:
+        raise ValueError("weights and counts must be 1-d arrays of equal length")
+    out = np.zeros(4, dtype=np.float64)
+    _check(load().dls_mc_estimate(w.ctypes.data, c.ctypes.data, int(w.shape[0]), float(n_k), out.ctypes.data),
+           "dls_mc_estimate")
+    return {"knuth": float(out[0]), "knuth_se": float(out[1]), "ratio": float(out[2]),
+            "mean_completions_weighted": float(out[3])}

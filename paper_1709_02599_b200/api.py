@@ -1,7 +1,6 @@
 """User-level calls over the C ABI (marshalling only; the search is the CUDA kernel)."""
 from __future__ import annotations
 
-import math
 from typing import Optional
 
 import numpy as np
@@ -16,10 +15,8 @@ def default_split_depth(n: int, symmetric: bool = False, fixed_first_row: bool =
 
 def first_row_multiplier(n: int, symmetric: bool = False) -> int:
     """Full count / first-row-fixed count: N! for DLS, (N/2)!*2^(N/2) for
-    vertically symmetric DLS (reading R3)."""
-    if symmetric:
-        return math.factorial(n // 2) * 2 ** (n // 2) if n % 2 == 0 else 0
-    return math.factorial(n)
+    vertically symmetric DLS (reading R3); computed by the library."""
+    return B.dls_scale_total(n, 0, symmetric)[1]
 
 
 def count_squares(n: int, symmetric: bool = False, fixed_first_row: bool = True,
@@ -31,7 +28,7 @@ def count_squares(n: int, symmetric: bool = False, fixed_first_row: bool = True,
     out = {"n": n, "symmetric": symmetric, "fixed_first_row": fixed_first_row, "depth": d,
            "n_prefix": int(pre.shape[0]), "count": total, "nodes": nodes}
     if fixed_first_row:
-        out["total_all_first_rows"] = total * first_row_multiplier(n, symmetric)
+        out["total_all_first_rows"] = B.dls_scale_total(n, total, symmetric)[0]
     return out
 
 

@@ -95,11 +95,7 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_STEP_V2
 #define DLS_STEP_V2 1
 #endif
-// DLS_STEP_V3=1 (needs V2): the stack slot is loaded only by lanes that do not
-// descend (0 otherwise), which makes two more selects of the step plain ORs / subtractions
-#ifndef DLS_STEP_V3
-#define DLS_STEP_V3 0
-#endif
+
 // A closure round (every lane evaluates its newest event) starts once this many
 // lanes of the warp hold one (A/B: profiles/r2_ab_close_min.log)
 constexpr int kCloseMinLanes = 24;
@@ -1178,27 +1174,17 @@ dls_search_kernel(const __grid_constant__ Params p) {
         for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
             const bool dn = cur != 0u;
             uint32_t sp;                                   // L of level lvl-1
-#if DLS_STEP_V3
-            // loaded only when the step does not descend (else 0: then bb = sibs = 0)
-            if constexpr (kSS == 0)
-                asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.shared.u8 %0, [%1];\n\t}"
-                             : "=&r"(sp) : "r"(one * d_stk + xq), "r"(cur));
-            else
-                asm volatile("{\n\t.reg .pred q;\n\tsetp.eq.s32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t@q ld.shared.u16 %0, [%1];\n\t}"
-                             : "=&r"(sp) : "r"((xq << kSS) + d_stk), "r"(cur));
-#else
             if constexpr (kSS == 0)
                 asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(one * d_stk + xq));
             else
                 asm volatile("ld.shared.u16 %0, [%1];" : "=r"(sp) : "r"((xq << kSS) + d_stk));
-#endif
             const uint32_t bb = sp & (0u - sp);            // its lowest bit: the value assigned there
             const uint32_t sibs = sp - bb;                 // L &= L-1
 #if DLS_STEP_V2
             // the level this step (re)assigns holds X: level lvl's candidates on a
             // descend, the untried siblings of level lvl-1 otherwise; empty =
             // plain backtrack.  One select, one lowest-bit isolation.
-            const uint32_t X = DLS_STEP_V3 ? (cur | sibs) : (dn ? cur : sibs);
+            const uint32_t X = dn ? cur : sibs;
             const bool adv = X != 0u;
             const uint32_t x = X & (0u - X);
             DLS_CHECK(xq >= fl_sa && xq <= fl_sa + ((uint32_t)(L + 1) << 10) && (!dn || xq <= fl_sa + ((uint32_t)L << 10)) &&
@@ -1227,13 +1213,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
 #if DLS_STEP_V2
             if constexpr (Geo<N, VS>::LAYOUT == 3) {
                 uint32_t d = x;
-                if (DLS_STEP_V3 || !dn) d = x - bb;
+                if (!dn) d = x - bb;
                 st.toggle_d(f, cs, d);                     // mark / unmark
             } else if constexpr (VS) {
-                st.toggle(f, x, (DLS_STEP_V3 || !dn) ? bb : 0u);
+                st.toggle(f, x, dn ? 0u : bb);
             } else {
                 uint32_t d = x;
-                if (DLS_STEP_V3 || !dn) d = x - bb;
+                if (!dn) d = x - bb;
                 st.toggle_d(f, d, d);
             }
             const uint32_t c = st.cand(cs);

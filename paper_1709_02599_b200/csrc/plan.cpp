@@ -10,6 +10,7 @@
 //
 // The planner only tracks how many cells of each unit are assigned (never
 // values), as the paper prescribes.
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -181,3 +182,45 @@ extern "C" int dls_plan(int n, int symmetric, int fixed_first_row, int32_t *out_
 }
 
 extern "C" const char *dls_last_error(void) { return dls::get_error(); }
+
+extern "C" int dls_scale_total(int n, int symmetric, uint64_t count_fixed, uint64_t *out128, uint64_t *out_multiplier) {
+    if (n < 1 || n > DLS_MAX_ORDER) { dls::set_error("dls_scale_total: order out of range"); return DLS_E_ARG; }
+    uint64_t m = 1;
+    if (symmetric) {
+        if (n % 2) {
+            m = 0;                                   // no vertically symmetric square of odd order (R6)
+        } else {
+            for (int k = 2; k <= n / 2; ++k) m *= (uint64_t)k;      // (N/2)!
+            m <<= n / 2;                                            // * 2^(N/2)
+        }
+    } else {
+        for (int k = 2; k <= n; ++k) m *= (uint64_t)k;              // N!
+    }
+    if (out_multiplier) *out_multiplier = m;
+    if (out128) {
+        const unsigned __int128 p = (unsigned __int128)count_fixed * (unsigned __int128)m;
+        out128[0] = (uint64_t)p;
+        out128[1] = (uint64_t)(p >> 64);
+    }
+    return DLS_OK;
+}
+
+extern "C" int dls_mc_estimate(const double *weights, const uint64_t *counts, int64_t n_samples, double n_k, double *out) {
+    if (!weights || !counts || !out || n_samples < 1) { dls::set_error("dls_mc_estimate: bad arguments"); return DLS_E_ARG; }
+    long double sw = 0, swc = 0;
+    for (int64_t s = 0; s < n_samples; ++s) {
+        sw += weights[s];
+        swc += (long double)weights[s] * (long double)counts[s];
+    }
+    const long double mean = swc / n_samples;
+    long double ss = 0;
+    for (int64_t s = 0; s < n_samples; ++s) {
+        const long double d = (long double)weights[s] * (long double)counts[s] - mean;
+        ss += d * d;
+    }
+    out[0] = (double)mean;
+    out[1] = n_samples > 1 ? (double)sqrtl(ss / (n_samples - 1) / n_samples) : __builtin_nan("");
+    out[2] = sw > 0 ? (double)(n_k * swc / sw) : 0.0;
+    out[3] = sw > 0 ? (double)(swc / sw) : 0.0;
+    return DLS_OK;
+}

@@ -49,13 +49,10 @@ def estimate(n, k, samples, seed, nk=None):
         cs.append(c)
         wc.append(w * c)
     t_s = time.perf_counter() - t
-    wc = np.array(wc, dtype=np.float64)
-    ws = np.array(ws, dtype=np.float64)
-    knuth = wc.mean()
-    knuth_se = wc.std(ddof=1) / math.sqrt(len(wc)) if len(wc) > 1 else float("nan")
-    ratio = nk * wc.sum() / ws.sum() if ws.sum() > 0 else 0.0
+    est = D.dls_mc_estimate(ws, cs, float(nk))       # mean / standard error / ratio form (C ABI)
+    knuth, knuth_se, ratio = est["knuth"], est["knuth_se"], est["ratio"]
     return {"n": n, "k": k, "samples": samples, "seed": seed, "N_k": nk, "knuth": knuth, "knuth_se": knuth_se,
-            "ratio": ratio, "mean_completions_weighted": wc.sum() / ws.sum() if ws.sum() else 0.0,
+            "ratio": ratio, "mean_completions_weighted": est["mean_completions_weighted"],
             "seconds_N_k": t_nk, "seconds_samples": t_s, "completions": [int(x) for x in cs]}
 
 

@@ -219,3 +219,37 @@ def test_binding_validates_buffers():
         B.dls_count(7, 11, recs, out_counts=np.zeros(3, np.uint64))
     with pytest.raises(ValueError):
         B.dls_emit(7, 11, recs, np.zeros((5, 49), np.int8))
+
+
+@pytest.mark.parametrize("n", range(1, 11))
+def test_scale_total_multipliers(n):
+    """dls_scale_total: N! for DLS, (N/2)! 2^(N/2) for vertical symmetry (R3,
+    pinned against the oracle's brute force in tests/test_oracle.py), 128-bit product."""
+    import math
+    tot, m = B.dls_scale_total(n, 12345678901234567, False)
+    assert m == math.factorial(n) and tot == 12345678901234567 * math.factorial(n)
+    tot, m = B.dls_scale_total(n, 987654321987, True)
+    want = math.factorial(n // 2) * 2 ** (n // 2) if n % 2 == 0 else 0
+    assert m == want == oracle.vs_first_row_multiplier(n) and tot == 987654321987 * want
+
+
+def test_scale_total_reproduces_paper_totals():
+    """5 056 994 653 507 584 x 9! = 1 835 082 219 864 832 081 920 (needs 128 bits)."""
+    tot, m = B.dls_scale_total(9, 5056994653507584, False)
+    assert m == 362880 and tot == 5056994653507584 * 362880 and tot > 2 ** 64
+    tot8, _ = B.dls_scale_total(8, 7447587840, False)
+    assert tot8 == 7447587840 * 40320
+
+
+def test_mc_estimate_arithmetic():
+    """dls_mc_estimate against the same sums written with numpy (Section 5.3)."""
+    rng = np.random.default_rng(7)
+    w = rng.integers(1, 50, 40).astype(np.float64) * 1e3
+    c = rng.integers(0, 10 ** 9, 40).astype(np.uint64)
+    r = B.dls_mc_estimate(w, c, 1.5e6)
+    wc = w * c.astype(np.float64)
+    assert r["knuth"] == pytest.approx(wc.mean(), rel=1e-12)
+    assert r["knuth_se"] == pytest.approx(wc.std(ddof=1) / np.sqrt(len(wc)), rel=1e-12)
+    assert r["ratio"] == pytest.approx(1.5e6 * wc.sum() / w.sum(), rel=1e-12)
+    assert r["mean_completions_weighted"] == pytest.approx(wc.sum() / w.sum(), rel=1e-12)
+    assert np.isnan(B.dls_mc_estimate(w[:1], c[:1], 1.0)["knuth_se"])
