@@ -535,11 +535,16 @@ struct Close<N, VS, 0> : CloseBase<N, VS> {
                 }
             w = make_uint4(m.C0, m.C1, m.R0, m.R1);
         }
+        const uint32_t c = eval_cols(w.x, w.y, ((rsel ? w.w : w.z) >> p.cl_rshift) & 0xFFu, p);
+        return ok ? c : 0u;
+    }
+    // the count from the column words and row r1's field (8-byte events, CROW
+    // kernels: row r1 has no searched cell, its field is a per-workunit constant)
+    __device__ __forceinline__ static uint32_t eval_cols(uint32_t c0, uint32_t c1, uint32_t rowf, const Params &p) {
         uint32_t f[B::EM];
 #pragma unroll
-        for (int k = 0; k < B::EM; ++k) f[k] = prmt(w.x, w.y, p.cl_sel[k]) & 0xFFu;
-        const uint32_t c = B::count(f, ((rsel ? w.w : w.z) >> p.cl_rshift) & 0xFFu, p);
-        return ok ? c : 0u;
+        for (int k = 0; k < B::EM; ++k) f[k] = prmt(c0, c1, p.cl_sel[k]) & 0xFFu;
+        return B::count(f, rowf, p);
     }
 };
 
@@ -798,7 +803,10 @@ __device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, 
 // 9- / 10-bit-field layouts, whose larger state needs up to 72 registers
 __host__ __device__ constexpr int max_lanes(int layout) { return layout < 2 ? 1024 : 896; }
 
-template <int N, bool VS, bool EMIT, bool CLOSE, bool LOOK = false>
+// CROW (byte layout, CLOSE): row r1 has no searched cell, so a closure event is
+// the two column words only (8 bytes, twice the event-stack depth) and row r1's
+// field is read from a per-lane byte written when the workunit is adopted
+template <int N, bool VS, bool EMIT, bool CLOSE, bool LOOK = false, bool CROW = false>
 __global__ void __launch_bounds__(max_lanes(Geo<N, VS>::LAYOUT), 1)
 dls_search_kernel(const __grid_constant__ Params p) {
     typedef Masks<N, VS> M;
@@ -823,9 +831,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // stack (16-byte aligned)
     const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)SST * (uint32_t)sizeof(SW);
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
-    const uint32_t CQSTR = (uint32_t)NT * (uint32_t)CL::EW * 4u;            // bytes per slot
+    static_assert(!CROW || (CLOSE && Geo<N, VS>::LAYOUT == 0 && !LOOK && !EMIT), "CROW: byte layout, closure");
+    constexpr uint32_t EW = CROW ? 2u : (uint32_t)CL::EW;                    // words per event
+    const uint32_t CQSTR = (uint32_t)NT * EW * 4u;                           // bytes per slot
     const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
-    const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * (uint32_t)CL::EW * 4u;
+    const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * EW * 4u;
+    uint8_t *const rowf_s = reinterpret_cast<uint8_t *>(cq_mem + (uint32_t)p.cl_cq * CQSTR);   // CROW: row r1's field per lane
     uint32_t cq_w = cq_lane0;          // shared address of this lane's next event slot
     // a lane's stack is deeper than k events iff cq_w > cq_lane0 + k * CQSTR
     const uint32_t cq_high = cq_lane0 + (uint32_t)(p.cl_cq - LY::GROUP) * CQSTR;
@@ -866,6 +877,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     constexpr bool kUni = DLS_UNIFIED && (Geo<N, VS>::LAYOUT == 0 || Geo<N, VS>::LAYOUT == 1 || Geo<N, VS>::LAYOUT == 3) &&
                           !LOOK && !EMIT && BLKW * 4 == 1024 && LY::SST_FIXED == 1024;
     constexpr int kSS = sizeof(SW) == 1 ? 0 : 1;     // a stack slot is 1024 << kSS bytes
+    static_assert(!CROW || kUni, "CROW kernels use the unified-address step");
     const uint32_t fl_sa = (uint32_t)__cvta_generic_to_shared(Fb);
     const uint32_t x_last = fl_sa + ((uint32_t)L << 10);          // above it: level L + 1
     const uint32_t d_stk = (uint32_t)__cvta_generic_to_shared(S) - (fl_sa << kSS);   // slot = (entry << kSS) + d_stk
@@ -906,7 +918,13 @@ dls_search_kernel(const __grid_constant__ Params p) {
     auto close_round = [&](uint32_t &cnt_) {
         const bool has = cq_w != cq_lane0;
         if (has) cq_w -= CQSTR;
-        const uint32_t k = CL::eval(reinterpret_cast<const uint32_t *>(cq_mem + (cq_w - cq_sa)), p, rsel);
+        uint32_t k;
+        if constexpr (CROW) {
+            const uint2 w2 = *reinterpret_cast<const uint2 *>(cq_mem + (cq_w - cq_sa));
+            k = CL::eval_cols(w2.x, w2.y, (uint32_t)rowf_s[tid], p);
+        } else {
+            k = CL::eval(reinterpret_cast<const uint32_t *>(cq_mem + (cq_w - cq_sa)), p, rsel);
+        }
         cnt_ += has ? k : 0u;
         const unsigned b = __ballot_sync(kFull, has);
         if (lane == 0) acc[6] += (u64)__popc(b);
@@ -1130,6 +1148,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
             if constexpr (CLOSE && Geo<N, VS>::LAYOUT >= 3) {
                 if (p.cl_swap_a >= 0) st.swap_rows(p.cl_swap_a, p.cl_swap_b);
             }
+            if constexpr (CROW) rowf_s[tid] = (uint8_t)((rsel ? st.R1 : st.R0) >> p.cl_rshift);
             cnt = 0;
             if (split == 0) {                  // a fresh workunit from the queue
                 if (!ok) {
@@ -1247,7 +1266,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
             ent32 += adv ? 1u : 0u;
             cur = adv ? c : 0u;
             xq = xn;
-            if constexpr (CLOSE) {
+            if constexpr (CROW) {
+                asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.u32 ev, %1, %2;\n\t"
+                             "@ev st.shared.v2.u32 [%0], {%4, %5};\n\t"
+                             "@ev mad.lo.u32 %0, %6, %3, %0;\n\t}"
+                             : "+r"(cq_w) : "r"(xn), "r"(x_last), "r"(CQSTR), "r"(st.C0), "r"(st.C1), "r"(one));
+            } else if constexpr (CLOSE) {
                 const uint4 w = CL::pack(st, rsel);
                 asm volatile("{\n\t.reg .pred ev;\n\tsetp.gt.u32 ev, %1, %2;\n\t"
                              "@ev st.shared.v4.u32 [%0], {%4, %5, %6, %7};\n\t"
@@ -1379,16 +1403,20 @@ dls_search_kernel(const __grid_constant__ Params p) {
 
 typedef void (*KernelFn)(Params);
 
+// close: 0 = plain search, 1 = closure, 2 = closure with column-only events (CROW)
 template <int N, bool VS>
-KernelFn kernel_for(bool emit, bool close, bool look = false) {
+KernelFn kernel_for(bool emit, int close, bool look = false) {
     if constexpr (N == 9 && !VS) {
         if (look && !emit) return close ? dls_search_kernel<N, VS, false, true, true> : dls_search_kernel<N, VS, false, false, true>;
+    }
+    if constexpr (DLS_UNIFIED && Geo<N, VS>::LAYOUT == 0) {
+        if (!emit && close == 2) return dls_search_kernel<N, VS, false, true, false, true>;
     }
     return emit ? dls_search_kernel<N, VS, true, false>
                 : (close ? dls_search_kernel<N, VS, false, true> : dls_search_kernel<N, VS, false, false>);
 }
 
-KernelFn pick_kernel(int n, bool vs, bool emit, bool close, bool look) {
+KernelFn pick_kernel(int n, bool vs, bool emit, int close, bool look) {
     switch (n) {
         case 1: return kernel_for<1, false>(emit, close);
         case 2: return vs ? kernel_for<2, true>(emit, close) : kernel_for<2, false>(emit, close);
@@ -1611,6 +1639,15 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
             if (open >> j & 1u) prm->cl_sel[k++] = sel(j);
         while (k < 10) prm->cl_sel[k++] = sel(pad);
         prm->close = 1;
+        {   // column-only events (CROW kernels): byte layout, unified step, no
+            // forced-cell walk, and no searched cell in row r1
+            bool row_const = lay == 0 && DLS_UNIFIED && nf == 0;
+            for (int s2 = depth; s2 < depth + l && row_const; ++s2)
+                if (plan.cells[s2] / n == r1) row_const = false;
+            if (const char *e16 = getenv("DLS_CLOSE_ROW16"))
+                if (atoi(e16) != 0) row_const = false;            // A/B: 16-byte events
+            if (row_const) prm->close = 2;
+        }
         prm->cl_swap_a = swap_a;
         prm->cl_swap_b = swap_b;
         prm->cl_min = kCloseMinLanes;
@@ -1719,18 +1756,19 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm, b
 constexpr int kCqMin = 8, kCqMinWide = 6, kCqMax = 16;
 
 // shared memory of a launch; cq = event slots per lane (0: no closure)
-size_t smem_bytes(int n, bool vs, int L, int nthreads, int cq, bool look = false) {
+size_t smem_bytes(int n, bool vs, int L, int nthreads, int cq, bool look = false, bool crow = false) {
     const int lay = layout_of(n, vs);
     const size_t sw = lay == 0 ? 1 : 2;                       // Layout::SW
     const size_t sst = (lay == 3 && DLS_UNIFIED) ? 1024 : nthreads;   // Layout::SST_FIXED
     const size_t stack = (size_t)(L + 1 + 4 / sw) * sst * sw;
     const size_t base = (size_t)(L + 2) * (look ? 40 : 32) * 32 + ((stack + 15) & ~(size_t)15);
-    const size_t ew = lay == 4 ? 8 : 4;                       // Close::EW
-    return base + (size_t)cq * nthreads * ew * 4;             // event stacks
+    const size_t ew = crow ? 2 : (lay == 4 ? 8 : 4);          // words per event
+    return base + (size_t)cq * nthreads * ew * 4 + (crow ? (size_t)nthreads : 0);   // event stacks (+ row bytes)
 }
 
 int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
-    const bool close = prm.close && prm.emit == nullptr;
+    const int close = prm.emit == nullptr ? prm.close : 0;      // 0 / 1 / 2 (column-only events)
+    const bool crow = close == 2;
     const bool look = prm.look && prm.emit == nullptr;
     KernelFn fn = pick_kernel(n, vs, prm.emit != nullptr, close, look);
     if (!fn) { dls::set_error("no kernel for this order"); return DLS_E_ARG; }
@@ -1747,13 +1785,13 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     int nthreads = max_lanes(lay);         // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
     // (a multiple of 64, so that the u16 stack's lanes keep distinct banks)
     const int cq_min = !close ? 0 : (lay == 0 ? kCqMin : kCqMinWide);
-    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, cq_min, look) > (size_t)smem_max) nthreads -= 64;
+    while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, cq_min, look, crow) > (size_t)smem_max) nthreads -= 64;
     int cq = cq_min;
     if (const char *ec = getenv("DLS_CLOSE_CQ")) cq = std::max(cq_min, atoi(ec));   // tuning: cap the depth
     else cq = kCqMax;
-    while (cq > cq_min && smem_bytes(n, vs, prm.L, nthreads, cq, look) > (size_t)smem_max) --cq;
+    while (cq > cq_min && smem_bytes(n, vs, prm.L, nthreads, cq, look, crow) > (size_t)smem_max) --cq;
     if (!close) cq = 0;
-    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, cq, look);
+    const size_t smem = smem_bytes(n, vs, prm.L, nthreads, cq, look, crow);
     if (smem > (size_t)smem_max) { dls::set_error("search state does not fit in shared memory"); return DLS_E_ARG; }
     if ((e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_fail(e, "cudaFuncSetAttribute");

@@ -123,12 +123,15 @@ def test_config4_vs8_full():
 
 
 def _read_golden(name):
+    """index -> (count, nodes) from the round-1 file and the stratified round-2
+    sample next to it (scripts/make_golden.py, make_golden_r2.py: oracle only)."""
     rows = {}
-    for line in open(golden(name)):
-        if line.startswith("#") or not line.strip():
-            continue
-        i, c, nd = line.split()[:3]
-        rows[int(i)] = (int(c), int(nd))
+    for fn in (name, name.replace(".txt", "_r2.txt")):
+        for line in open(golden(fn)):
+            if line.startswith("#") or not line.strip():
+                continue
+            i, c, nd = line.split()[:3]
+            rows[int(i)] = (int(c), int(nd))
     return rows
 
 
