@@ -1644,8 +1644,9 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
             bool row_const = lay == 0 && DLS_UNIFIED && nf == 0;
             for (int s2 = depth; s2 < depth + l && row_const; ++s2)
                 if (plan.cells[s2] / n == r1) row_const = false;
-            if (const char *e16 = getenv("DLS_CLOSE_ROW16"))
-                if (atoi(e16) != 0) row_const = false;            // A/B: 16-byte events
+            // opt-in until verified on the GPU (DLS_CLOSE_ROW8=1)
+            const char *e8 = getenv("DLS_CLOSE_ROW8");
+            if (!e8 || atoi(e8) == 0) row_const = false;
             if (row_const) prm->close = 2;
         }
         prm->cl_swap_a = swap_a;
