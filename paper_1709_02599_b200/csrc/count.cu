@@ -95,6 +95,11 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_STEP_V2
 #define DLS_STEP_V2 1
 #endif
+// steps between two looks at the event stacks in the kernels with 8-byte events
+// (their stacks are twice as deep)
+#ifndef DLS_GROUP8
+#define DLS_GROUP8 8
+#endif
 
 // A closure round (every lane evaluates its newest event) starts once this many
 // lanes of the warp hold one (A/B: profiles/r2_ab_close_min.log)
@@ -833,13 +838,14 @@ dls_search_kernel(const __grid_constant__ Params p) {
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
     static_assert(!CROW || (CLOSE && Geo<N, VS>::LAYOUT == 0 && !LOOK && !EMIT), "CROW: byte layout, closure");
     constexpr uint32_t EW = CROW ? 2u : (uint32_t)CL::EW;                    // words per event
+    constexpr int kGroup = CROW ? DLS_GROUP8 : LY::GROUP;                      // steps between looks at the event stacks
     const uint32_t CQSTR = (uint32_t)NT * EW * 4u;                           // bytes per slot
     const uint32_t cq_sa = (uint32_t)__cvta_generic_to_shared(cq_mem);
     const uint32_t cq_lane0 = cq_sa + (uint32_t)tid * EW * 4u;
     uint8_t *const rowf_s = reinterpret_cast<uint8_t *>(cq_mem + (uint32_t)p.cl_cq * CQSTR);   // CROW: row r1's field per lane
     uint32_t cq_w = cq_lane0;          // shared address of this lane's next event slot
     // a lane's stack is deeper than k events iff cq_w > cq_lane0 + k * CQSTR
-    const uint32_t cq_high = cq_lane0 + (uint32_t)(p.cl_cq - LY::GROUP) * CQSTR;
+    const uint32_t cq_high = cq_lane0 + (uint32_t)(p.cl_cq - kGroup) * CQSTR;
     const uint32_t cl_min = (uint32_t)p.cl_min;    // lanes holding an event that start a round
     const uint32_t rsel = (uint32_t)p.cl_rword;
 
@@ -937,8 +943,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
         // ------------------------------------------------ scheduling point
         if (CLOSE) {
             // every pending event belongs to the lane's current workunit: settle
-            // them before a lane can finish it or take another
-            close_drain(cnt);
+            // them before a lane finishes it (donated subtrees stay within the
+            // workunit, so donors and receivers need no drain)
+            if (__any_sync(kFull, pid >= 0 && lvl == 0 && cq_w != cq_lane0)) close_drain(cnt);
             if (pid >= 0 && cnt >= 0x80000000u) {
                 if (p.counts) atomicAdd(p.counts + (p.parent ? p.parent[pid] : (uint32_t)pid), (u64)cnt);
                 atomicAdd(acc + 0, (u64)cnt);
@@ -1188,9 +1195,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
         // x + k on the FMA pipe (one * k + x) or as a plain add
         const uint32_t one = DLS_FMA_ADDS ? p.one : 1u;
         auto addk = [&](uint32_t x, uint32_t k) { return one * k + x; };
-        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? LY::GROUP : 8)) {
+        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? kGroup : 8)) {
 #pragma unroll
-        for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
+        for (int s = 0; s < (CLOSE ? kGroup : 8); ++s) {
             const bool dn = cur != 0u;
             uint32_t sp;                                   // L of level lvl-1
             if constexpr (kSS == 0)
@@ -1291,9 +1298,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
         lvl = (int)((xq - fl_sa) >> 10);
         asm volatile("" ::: "memory");
         } else {
-        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? LY::GROUP : 8)) {
+        for (int s0 = 0; s0 < kBurst; s0 += (CLOSE ? kGroup : 8)) {
 #pragma unroll
-        for (int s = 0; s < (CLOSE ? LY::GROUP : 8); ++s) {
+        for (int s = 0; s < (CLOSE ? kGroup : 8); ++s) {
             const bool dn = cur != 0u;                     // descend: cell(lvl) has candidates
             const uint32_t b = cur & (0u - cur);          // isolate rightmost 1-bit
             const int t = dn ? lvl : lvl - 1;              // toggle at cell(t), then read cell(t+1)
@@ -1644,9 +1651,8 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
             bool row_const = lay == 0 && DLS_UNIFIED && nf == 0;
             for (int s2 = depth; s2 < depth + l && row_const; ++s2)
                 if (plan.cells[s2] / n == r1) row_const = false;
-            // opt-in until verified on the GPU (DLS_CLOSE_ROW8=1)
-            const char *e8 = getenv("DLS_CLOSE_ROW8");
-            if (!e8 || atoi(e8) == 0) row_const = false;
+            if (const char *e8 = getenv("DLS_CLOSE_ROW8"))
+                if (atoi(e8) == 0) row_const = false;             // A/B: 16-byte events
             if (row_const) prm->close = 2;
         }
         prm->cl_swap_a = swap_a;
@@ -1754,7 +1760,7 @@ int prepare(int n, int symmetric, int fixed_first_row, int depth, Params *prm, b
 
 // event slots per lane of the closure kernels: at least kCqMin (= the largest
 // GROUP + 2), at most kCqMax
-constexpr int kCqMin = 8, kCqMinWide = 6, kCqMax = 16;
+constexpr int kCqMin = 8, kCqMinWide = 6, kCqMax = 20;
 
 // shared memory of a launch; cq = event slots per lane (0: no closure)
 size_t smem_bytes(int n, bool vs, int L, int nthreads, int cq, bool look = false, bool crow = false) {
@@ -1785,7 +1791,7 @@ int launch(int n, bool vs, const Params &prm, cudaStream_t stream) {
     const int lay = layout_of(n, vs);
     int nthreads = max_lanes(lay);         // = the kernel's __launch_bounds__ (layouts 0, 1: fixed)
     // (a multiple of 64, so that the u16 stack's lanes keep distinct banks)
-    const int cq_min = !close ? 0 : (lay == 0 ? kCqMin : kCqMinWide);
+    const int cq_min = !close ? 0 : (crow ? DLS_GROUP8 + 2 : (lay == 0 ? kCqMin : kCqMinWide));
     while (lay >= 2 && nthreads > 64 && smem_bytes(n, vs, prm.L, nthreads, cq_min, look, crow) > (size_t)smem_max) nthreads -= 64;
     int cq = cq_min;
     if (const char *ec = getenv("DLS_CLOSE_CQ")) cq = std::max(cq_min, atoi(ec));   // tuning: cap the depth

@@ -324,6 +324,47 @@ def test_device_buffers_and_async_stats():
     assert total == want and int(out.sum()) == want
 
 
+def test_concurrent_streams_and_threads():
+    """Calls on different streams / from different host threads at once: the
+    search kernel is a cooperative launch (every warp of the grid must be resident
+    for its exit protocol), so concurrent launches run one after the other instead
+    of dead-locking, and every call returns the oracle's count."""
+    import threading
+    import torch
+    want7, want6 = oracle.count_all(7), oracle.count_all(6, vs=True)
+    d7, d6 = D.default_split_depth(7), D.default_split_depth(6, True)
+    dev7 = torch.from_numpy(D.dls_split(7, d7)).cuda()
+    dev6 = torch.from_numpy(D.dls_split(6, d6, True)).cuda()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    stats = [torch.zeros(B.DLS_STATS_WORDS, dtype=torch.int64, device="cuda") for _ in range(4)]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for k, s in enumerate(streams):
+            if k % 2 == 0:
+                D.dls_count_async(7, d7, dev7, None, stats[k], stream=s.cuda_stream)
+            else:
+                D.dls_count_async(6, d6, dev6, None, stats[k], True, stream=s.cuda_stream)
+        torch.cuda.synchronize()
+        for k in range(4):
+            assert int(stats[k][0]) == (want7 if k % 2 == 0 else want6) and int(stats[k][2]) == 0
+    got = {}
+
+    def work(k):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        if k % 2 == 0:
+            got[k] = D.dls_count(7, d7, dev7, stream=s.cuda_stream)[0]
+        else:
+            got[k] = D.dls_count(6, d6, dev6, True, stream=s.cuda_stream)[0]
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert got == {0: want7, 1: want6, 2: want7, 3: want6}
+
+
 def test_repeatable():
     n = 8
     d = D.default_split_depth(n)
