@@ -579,12 +579,16 @@ struct Close<N, VS, 1> : CloseBase<N, VS> {
                 }
             w = make_uint4(m.C0, m.C1, m.R0, m.R1);
         }
+        const uint32_t c = eval_cols(w.x, w.y, (rsel ? w.w : w.z) >> p.cl_rshift, p);
+        return ok ? c : 0u;
+    }
+    // the count from the column words and row r1's field (8-byte events, CROW kernels)
+    __device__ __forceinline__ static uint32_t eval_cols(uint32_t c0, uint32_t c1, uint32_t rowf, const Params &p) {
         uint32_t f[B::EM];
 #pragma unroll
         for (int k = 0; k < B::EM; ++k)
-            f[k] = (uint32_t)((((u64)w.y << 32) | w.x) >> p.cl_sel[k]) & ((1u << G::CF) - 1u);
-        const uint32_t c = B::count(f, ((rsel ? w.w : w.z) >> p.cl_rshift) & ((1u << G::RF) - 1u), p);
-        return ok ? c : 0u;
+            f[k] = (uint32_t)((((u64)c1 << 32) | c0) >> p.cl_sel[k]) & ((1u << G::CF) - 1u);
+        return B::count(f, rowf & ((1u << G::RF) - 1u), p);
     }
 };
 
@@ -808,7 +812,7 @@ __device__ __noinline__ void emit_square(const Params &p, int pid, const SW *S, 
 // 9- / 10-bit-field layouts, whose larger state needs up to 72 registers
 __host__ __device__ constexpr int max_lanes(int layout) { return layout < 2 ? 1024 : 896; }
 
-// CROW (byte layout, CLOSE): row r1 has no searched cell, so a closure event is
+// CROW (layouts 0 and 1, CLOSE): row r1 has no searched cell, so a closure event is
 // the two column words only (8 bytes, twice the event-stack depth) and row r1's
 // field is read from a per-lane byte written when the workunit is adopted
 template <int N, bool VS, bool EMIT, bool CLOSE, bool LOOK = false, bool CROW = false>
@@ -836,7 +840,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // stack (16-byte aligned)
     const uint32_t stack_bytes = (uint32_t)(L + 1 + LY::PACK) * (uint32_t)SST * (uint32_t)sizeof(SW);
     char *const cq_mem = stk + ((stack_bytes + 15u) & ~15u);
-    static_assert(!CROW || (CLOSE && Geo<N, VS>::LAYOUT == 0 && !LOOK && !EMIT), "CROW: byte layout, closure");
+    static_assert(!CROW || (CLOSE && Geo<N, VS>::LAYOUT <= 1 && !LOOK && !EMIT), "CROW: byte / word-field layout, closure");
     constexpr uint32_t EW = CROW ? 2u : (uint32_t)CL::EW;                    // words per event
     constexpr int kGroup = CROW ? DLS_GROUP8 : LY::GROUP;                      // steps between looks at the event stacks
     const uint32_t CQSTR = (uint32_t)NT * EW * 4u;                           // bytes per slot
@@ -1416,7 +1420,7 @@ KernelFn kernel_for(bool emit, int close, bool look = false) {
     if constexpr (N == 9 && !VS) {
         if (look && !emit) return close ? dls_search_kernel<N, VS, false, true, true> : dls_search_kernel<N, VS, false, false, true>;
     }
-    if constexpr (DLS_UNIFIED && Geo<N, VS>::LAYOUT == 0) {
+    if constexpr (DLS_UNIFIED && Geo<N, VS>::LAYOUT <= 1) {
         if (!emit && close == 2) return dls_search_kernel<N, VS, false, true, false, true>;
     }
     return emit ? dls_search_kernel<N, VS, true, false>
@@ -1648,7 +1652,7 @@ int closure_level(const dls::Plan &plan, int depth, Params *prm) {
         prm->close = 1;
         {   // column-only events (CROW kernels): byte layout, unified step, no
             // forced-cell walk, and no searched cell in row r1
-            bool row_const = lay == 0 && DLS_UNIFIED && nf == 0;
+            bool row_const = lay <= 1 && DLS_UNIFIED && nf == 0;
             for (int s2 = depth; s2 < depth + l && row_const; ++s2)
                 if (plan.cells[s2] / n == r1) row_const = false;
             if (const char *e8 = getenv("DLS_CLOSE_ROW8"))
