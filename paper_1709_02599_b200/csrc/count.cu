@@ -916,11 +916,12 @@ dls_search_kernel(const __grid_constant__ Params p) {
     // [4] lane-bursts -- keeps them out of the registers of the search loop
     // [5] (lane 0 only): ns between pool polls of this warp while idle (0: not waiting)
     // [6] closure events evaluated
-    __shared__ u64 wacc[32][7];
+    // [7] the work queue has run dry (warp-uniform flag, kept here rather than in a
+    //     register that would be live -- and spilled -- across the DFS loop)
+    __shared__ u64 wacc[32][8];
     u64 *const acc = wacc[tid >> 5];
-    if (lane < 7) acc[lane] = 0;
+    if (lane < 8) acc[lane] = 0;
     __syncwarp();
-    bool qempty = false;
     const u64 n_prefix = (u64)p.n_prefix;
 
     // One round: every lane holding an event evaluates and pops its newest one;
@@ -968,6 +969,7 @@ dls_search_kernel(const __grid_constant__ Params p) {
         bool adopt = false;
         int split = 0;
         uint32_t rest = 0;
+        bool qempty = *reinterpret_cast<volatile u64 *>(acc + 7) != 0ull;
         if (!qempty) {
             const unsigned idle = __ballot_sync(kFull, pid < 0);
             if (idle) {
@@ -977,7 +979,10 @@ dls_search_kernel(const __grid_constant__ Params p) {
                 base = __shfl_sync(kFull, base, leader);
                 if (base + (u64)__popc(idle) >= n_prefix) {
                     qempty = true;
-                    if (lane == leader) stamp_first(pool, kStampQEmpty);
+                    if (lane == leader) {
+                        acc[7] = 1ull;
+                        stamp_first(pool, kStampQEmpty);
+                    }
                 }
                 if (pid < 0) {
                     const u64 my = base + (u64)__popc(idle & lt_mask);
