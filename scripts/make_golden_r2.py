@@ -49,7 +49,10 @@ def main():
     ap.add_argument("--workers", type=int, default=5)
     ap.add_argument("--dls9", type=int, default=10)
     ap.add_argument("--vs10", type=int, default=24)
+    ap.add_argument("--indices-dls9", default="", help="comma-separated seeded-prefix indices to add (e.g. the GPU's min / max counts)")
+    ap.add_argument("--indices-vs10", default="")
     a = ap.parse_args()
+    extra = {"dls9": [int(x) for x in a.indices_dls9.split(",") if x], "vs10": [int(x) for x in a.indices_vs10.split(",") if x]}
     jobs = []
     pre9 = synth.diagonal_prefixes(synth.SEED_DLS9, 9, synth.N_DLS9)
     pre10 = synth.diagonal_prefixes(synth.SEED_VS10, 10, synth.N_VS10, vs=True)
@@ -64,8 +67,8 @@ def main():
                 f.write("# Written by scripts/make_golden_r2.py: oracle.count on synth.diagonal_prefixes("
                         "seed=%d, n=%d, vs=%s) records,\n# one index per equal-width stratum "
                         "(default_rng(2026)).\n# index count nodes oracle_seconds\n" % (seed, n, vs))
-        for i in strata(len(pre), k, set(R1[tag])):
-            if i not in done:
+        for i in (strata(len(pre), k, set(R1[tag])) if k > 0 else []) + extra[tag]:
+            if i not in done and i not in R1[tag]:
                 jobs.append((tag, n, vs, i, pre[i]))
     with Pool(a.workers) as pool:
         for tag, idx, c, nodes, sec in pool.imap_unordered(job, jobs, chunksize=1):
