@@ -100,6 +100,11 @@ constexpr int kBurst = DLS_BURST;   // DFS steps between warp scheduling points
 #ifndef DLS_GROUP8
 #define DLS_GROUP8 8
 #endif
+// kernels with 8-byte events: 1 = closure rounds start when a stack nears its
+// depth (one vote per look), 0 = when enough lanes hold an event (a reduction)
+#ifndef DLS_ROUNDS_ON_FULL
+#define DLS_ROUNDS_ON_FULL 1
+#endif
 
 // A closure round (every lane evaluates its newest event) starts once this many
 // lanes of the warp hold one (A/B: profiles/r2_ab_close_min.log)
@@ -1201,6 +1206,8 @@ dls_search_kernel(const __grid_constant__ Params p) {
         // ---- unified-address step (same step as below, see DLS_UNIFIED)
         asm volatile("" ::: "memory");           // the stack is accessed through asm from here
         uint32_t xq = fl_sa + ((uint32_t)lvl << 10);   // entry of transition lvl == slot of level lvl-1 (+ d_stk)
+        // address of the stack slot of level lvl-1 (= slot `lvl`), carried from step to step
+        uint32_t sa = (xq << kSS) + d_stk;
         // x + k on the FMA pipe (one * k + x) or as a plain add
         const uint32_t one = DLS_FMA_ADDS ? p.one : 1u;
         auto addk = [&](uint32_t x, uint32_t k) { return one * k + x; };
@@ -1210,9 +1217,9 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const bool dn = cur != 0u;
             uint32_t sp;                                   // L of level lvl-1
             if constexpr (kSS == 0)
-                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(one * d_stk + xq));
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(sp) : "r"(sa));
             else
-                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(sp) : "r"((xq << kSS) + d_stk));
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(sp) : "r"(sa));
             const uint32_t bb = sp & (0u - sp);            // its lowest bit: the value assigned there
             const uint32_t sibs = sp - bb;                 // L &= L-1
 #if DLS_STEP_V2
@@ -1273,10 +1280,11 @@ dls_search_kernel(const __grid_constant__ Params p) {
             const uint32_t c = st.cand(cs);
             const uint32_t xn = max(adv ? addk(xt, 1024u) : xt, fl_sa);   // level nl = max(t + adv, 0)
 #endif
+            sa = (xn << kSS) + d_stk;                      // the slot the step writes and the next one reads
             if constexpr (kSS == 0) {
-                if (adv) asm volatile("st.shared.u8 [%0], %1;" :: "r"(one * d_stk + xn), "r"(X));
+                if (adv) asm volatile("st.shared.u8 [%0], %1;" :: "r"(sa), "r"(X));
             } else {
-                if (adv) asm volatile("st.shared.u16 [%0], %1;" :: "r"((xn << kSS) + d_stk), "r"(X));
+                if (adv) asm volatile("st.shared.u16 [%0], %1;" :: "r"(sa), "r"(X));
             }
             if (!CLOSE) cnt32 += xn > x_last ? 1u : 0u;
             ent32 += adv ? 1u : 0u;
@@ -1295,7 +1303,18 @@ dls_search_kernel(const __grid_constant__ Params p) {
                              : "+r"(cq_w) : "r"(xn), "r"(x_last), "r"(CQSTR), "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w), "r"(one));
             }
         }
-            if constexpr (CLOSE) {
+            if constexpr (CROW && DLS_ROUNDS_ON_FULL) {
+                // deep stacks (8-byte events): the look is one vote -- rounds start
+                // when some stack nears its depth and go on while enough lanes hold
+                // an event (by then most do)
+                if (__any_sync(kFull, cq_w > cq_high)) {
+                    unsigned red;
+                    do {
+                        close_round(cnt32);
+                        red = __reduce_add_sync(kFull, (cq_w != cq_lane0 ? 1u : 0u) + (cq_w > cq_high ? 1024u : 0u));
+                    } while (red >= cl_min);
+                }
+            } else if constexpr (CLOSE) {
                 const unsigned pk = (cq_w != cq_lane0 ? 1u : 0u) + (cq_w > cq_high ? 1024u : 0u);
                 unsigned red = __reduce_add_sync(kFull, pk);
                 if (red >= cl_min) {
